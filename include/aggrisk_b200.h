@@ -1,0 +1,160 @@
+/*
+ * aggrisk_b200.h -- C ABI of the B200 aggregate-analysis engine
+ * (libaggrisk_b200.so, built from paper_1308_2066_b200/csrc/).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types cross this boundary
+ * (`void *stream` is a cudaStream_t, 0 = the legacy default stream).
+ * Every entry point returns an `are_status` and records a thread-local
+ * message readable through are_last_error().
+ *
+ * The reference seam this library replaces is the backend module's
+ * `run_trials` (reference: pkg/src/aggrisk/engine/_kernel.pyx:17-30, chosen
+ * by _backend_module at pkg/src/aggrisk/engine/__init__.py:147-148 and
+ * called from _run_layer.task :179-191 and analyse_trial :313-319), together
+ * with the table build it consumes (TableSet.from_elts, tables.py:95-117)
+ * and the order statistics downstream of it (metrics.py:29-115).  The
+ * one-to-one mapping is given per function below; INTEGRATION.md shows the
+ * ctypes binding a maintainer adds on the reference side.
+ *
+ * Ownership: the caller owns every host buffer and every device buffer it
+ * passes in; the library only borrows them for the duration of the call.
+ * Handles (are_tables_t, are_plan_t) own device memory and are freed with
+ * their *_free call.  Handles are immutable after construction and may be
+ * used from several host threads at once (the reference kernel is
+ * re-entrant; so is this library).
+ */
+#ifndef AGGRISK_B200_H
+#define AGGRISK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ARE_OK = 0,
+    ARE_EINVAL = 1,      /* reference raises ValueError           */
+    ARE_ERANGE = 2,      /* reference raises EventOutOfRangeError */
+    ARE_ECUDA = 3,       /* CUDA runtime failure (no device, launch error ...) */
+    ARE_ENOMEM = 4,      /* device or pinned-host allocation failed */
+    ARE_EINDEX = 5       /* reference raises IndexError (bad selection row) */
+} are_status;
+
+#define ARE_MAX_TABLES 256 /* reference: _kernel.pyx:14 (MAX_TABLES) */
+
+/* K2 variant selector for are_simulate_* */
+#define ARE_VARIANT_AUTO 0   /* hot-set kernel when zero-skip is exact, else dense */
+#define ARE_VARIANT_HOTSET 1 /* force the hot-set kernel (fails if not exact)      */
+#define ARE_VARIANT_DENSE 2  /* force the dense direct-access kernel              */
+
+typedef struct are_tables_s *are_tables_t;
+typedef struct are_plan_s *are_plan_t;
+
+typedef struct {
+    int64_t n_sel;            /* selected tables (accumulation order)            */
+    int64_t row_len;          /* catalog_size + 1                                 */
+    int64_t hot_events;       /* events with >= 1 non-zero loss in the selection  */
+    int64_t entries;          /* non-zero (event, table) pairs                    */
+    int64_t overflow_entries; /* entries beyond the first per event               */
+    int64_t filter_bits;      /* bits of the shared-memory hot filter             */
+    int64_t device_bytes;     /* device memory owned by the plan                  */
+    int32_t zero_skip_exact;  /* every fin_j(+-0) == +-0 (hot-set kernel usable)  */
+    int32_t smem_bytes;       /* dynamic shared memory of the hot-set kernel      */
+} are_plan_info_t;
+
+/* ---- library / device ------------------------------------------------ */
+const char *are_last_error(void);
+int are_version(void);
+int are_device_count(int *n);
+int are_select_device(int ordinal);
+int are_device_sm_count(int *n);
+/* Number of kernels this library launched in the calling process. */
+int64_t are_launch_count(void);
+/* Pin / unpin a caller-owned host buffer (cudaHostRegister) so the host
+ * entry points copy from it without staging. */
+int are_host_register(void *ptr, int64_t bytes);
+int are_host_unregister(void *ptr);
+
+/* ---- K1: ELT ingestion (replaces TableSet.from_elts, tables.py:95-117) -- */
+/* Dense stacked float64 (n_tables, row_len), row-major, as TableSet.stacked. */
+int are_tables_from_dense(const double *stacked, int64_t n_tables, int64_t row_len,
+                          are_tables_t *out);
+/* Sparse ELT records: table i owns ids/losses[table_offsets[i] .. [i+1]).
+ * Ids must lie in [1, row_len-1] (else ARE_ERANGE, tables.py:111-114) and be
+ * unique within a table. */
+int are_tables_from_records(const uint32_t *ids, const double *losses,
+                            const int64_t *table_offsets, int64_t n_tables,
+                            int64_t row_len, are_tables_t *out);
+int are_tables_info(are_tables_t t, int64_t *n_tables, int64_t *row_len,
+                    int64_t *device_bytes);
+/* Copy dense row `row` (row_len doubles) back to the host. */
+int are_tables_read_row(are_tables_t t, int64_t row, double *host_out);
+int are_tables_free(are_tables_t t);
+
+/* ---- selection + financial terms (TableSet.selection_arrays, tables.py:133-153) */
+int are_plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel,
+                   const double *fin_rate, const double *fin_ret,
+                   const double *fin_lim, const double *fin_share,
+                   are_plan_t *out);
+int are_plan_info(are_plan_t p, are_plan_info_t *info);
+int are_plan_free(are_plan_t p);
+
+/* ---- K2: per-trial simulation (replaces run_trials, _kernel.pyx:17-119) --
+ * Trials [first, last) of a YET whose offsets are int64 (length T+1) and
+ * whose event ids are uint32.  out[t] (float64) is written for t in range.
+ *
+ * Device form: d_event_ids[i] is occurrence i, d_offsets[t] is offset t,
+ * d_out[t] is trial t (pointers may be offset by the caller as usual).
+ * Launches on `stream`; does not synchronise.  Event ids >= row_len set a
+ * device error flag that the next are_check_errors() reports (ARE_ERANGE). */
+int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ,
+                        const int64_t *d_offsets, int64_t n_trials,
+                        int64_t first, int64_t last,
+                        double occ_ret, double occ_lim, double agg_ret, double agg_lim,
+                        double *d_out, void *stream, int32_t variant);
+int are_check_errors(are_plan_t p, void *stream);
+
+/* Host form: host ids/offsets/out; the library streams trial chunks to the
+ * device (overlapping copies with K2) and returns when `out` is filled.
+ * *lookups = n_sel * (offsets[last] - offsets[first]) exactly as the
+ * reference counts them (_kernel.pyx:77). */
+int are_simulate_host(are_plan_t p, const uint32_t *event_ids, int64_t n_occ,
+                      const int64_t *offsets, int64_t n_trials,
+                      int64_t first, int64_t last,
+                      double occ_ret, double occ_lim, double agg_ret, double agg_lim,
+                      double *out, int64_t *lookups, int32_t variant);
+
+/* Drop-in for the reference run_trials with its exact argument list
+ * (_kernel.pyx:17-30).  `chunk` and `scratch` keep their reference meaning
+ * for validation only (chunk > 0 requires scratch_len >= chunk,
+ * _kernel.pyx:51-52); results do not depend on them.  Uploads `stacked`
+ * on every call -- use the tables/plan handles to keep it resident. */
+int are_run_trials(const uint32_t *event_ids, int64_t n_occ,
+                   const int64_t *offsets, int64_t n_offsets,
+                   const double *stacked, int64_t n_tables, int64_t row_len,
+                   const int64_t *rows, int64_t n_sel,
+                   const double *fin_rate, const double *fin_ret,
+                   const double *fin_lim, const double *fin_share,
+                   double occ_ret, double occ_lim, double agg_ret, double agg_lim,
+                   int64_t chunk, int64_t first_trial, int64_t last_trial,
+                   double *out, int64_t scratch_len, int64_t *lookups);
+
+/* ---- K3: order statistics (replaces pml/tvar/ep_curve, metrics.py:29-115) --
+ * For each return period rp[r]: k = n - floor(n / rp) (metrics.py:40),
+ * pml[r] = k-th smallest loss, tvar[r] = mean of the top n-k+1 losses.
+ * Requires 1 < rp <= n (ARE_EINVAL otherwise, metrics.py:36-39). */
+int are_order_stats_device(const double *d_losses, int64_t n,
+                           const double *rps, int64_t n_rp,
+                           double *pml_out, double *tvar_out, void *stream);
+int are_order_stats_host(const double *losses, int64_t n,
+                         const double *rps, int64_t n_rp,
+                         double *pml_out, double *tvar_out);
+/* portfolio_rollup (metrics.py:118-133): d_out[t] = ((y0[t] + y1[t]) + ...). */
+int are_rollup_device(const double *const *d_ylts, int64_t n_layers, int64_t n,
+                      double *d_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AGGRISK_B200_H */

@@ -1,0 +1,654 @@
+// extern "C" surface of libaggrisk_b200.so (include/aggrisk_b200.h) and the
+// host-side orchestration around K1/K2/K3: device handles, the chunked
+// host->device streaming pipeline for host-resident YETs, and argument
+// validation with the reference's error behaviour.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "k1_ingest.cuh"
+#include "k2_trials.cuh"
+#include "k3_order_stats.cuh"
+
+namespace are {
+
+static thread_local std::string t_err;
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string &msg) { t_err = msg; }
+int fail(int code, const std::string &msg) {
+    t_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char *what) {
+    t_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? ARE_ENOMEM : ARE_ECUDA;
+}
+
+// ---- per-device facts ------------------------------------------------------
+struct DeviceInfo {
+    int sms = 0;
+    int smem_optin = 0;
+    bool ready = false;
+};
+static std::mutex g_dev_mu;
+static DeviceInfo g_dev[64];
+
+static int use_device(int dev, DeviceInfo **out) {
+    if (dev < 0 || dev >= 64) return fail(ARE_EINVAL, "bad device ordinal");
+    ARE_CUDA(cudaSetDevice(dev));
+    std::lock_guard<std::mutex> g(g_dev_mu);
+    DeviceInfo &d = g_dev[dev];
+    if (!d.ready) {
+        int major = 0;
+        ARE_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+        if (major < 10)
+            return fail(ARE_ECUDA, "paper_1308_2066_b200 requires an sm_100 (B200) device");
+        ARE_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+        ARE_CUDA(cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        int rc = k2_prepare(dev);
+        if (rc) return rc;
+        d.ready = true;
+    }
+    *out = &d;
+    return ARE_OK;
+}
+
+static int current_device(int *dev) {
+    ARE_CUDA(cudaGetDevice(dev));
+    return ARE_OK;
+}
+
+}  // namespace are
+
+using namespace are;
+
+struct are_tables_s {
+    int device = 0;
+    int64_t n_tables = 0, row_len = 0;
+    double *d = nullptr;
+    std::atomic<int> refs{1};
+};
+
+struct are_plan_s {
+    int device = 0;
+    are_tables_s *tab = nullptr;
+    int64_t n_sel = 0;
+    int64_t *d_rows = nullptr;
+    Fin *d_fin = nullptr;
+    PlanBuffers pb;
+    int64_t nbits = 0;
+    int hash_mode = 0;
+    bool zero_skip = false;
+    unsigned int *d_err = nullptr;
+    size_t smem = 0;
+};
+
+static void tables_release(are_tables_s *t) {
+    if (t && t->refs.fetch_sub(1) == 1) {
+        cudaSetDevice(t->device);
+        cudaFree(t->d);
+        delete t;
+    }
+}
+
+// ---- host streaming workspace (one per device, grown on demand) -----------
+namespace are {
+struct Workspace {
+    std::mutex mu;
+    bool init = false;
+    cudaStream_t copy = nullptr, comp = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+    uint32_t *d_ids[2] = {nullptr, nullptr};
+    int64_t *d_off[2] = {nullptr, nullptr};
+    uint32_t *h_ids[2] = {nullptr, nullptr};  // pinned bounce buffers (pageable inputs)
+    int64_t *h_off[2] = {nullptr, nullptr};
+    int64_t cap_ids = 0, cap_off = 0;
+    double *d_out = nullptr;
+    int64_t cap_out = 0;
+    unsigned int *d_err = nullptr;
+};
+static Workspace g_ws[64];
+static constexpr int64_t CHUNK_OCC = 32ll << 20;  // 32 Mi occurrences (128 MiB of ids) per chunk
+
+static int ws_reserve(Workspace &w, int64_t ids, int64_t offs, int64_t outs, bool bounce) {
+    if (!w.init) {
+        ARE_CUDA(cudaStreamCreateWithFlags(&w.copy, cudaStreamNonBlocking));
+        ARE_CUDA(cudaStreamCreateWithFlags(&w.comp, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            ARE_CUDA(cudaEventCreateWithFlags(&w.copied[i], cudaEventDisableTiming));
+            ARE_CUDA(cudaEventCreateWithFlags(&w.consumed[i], cudaEventDisableTiming));
+        }
+        ARE_CUDA(cudaMalloc(&w.d_err, sizeof(unsigned int)));
+        w.init = true;
+    }
+    if (ids > w.cap_ids || offs > w.cap_off || (bounce && !w.h_ids[0])) {
+        ids = std::max(ids, w.cap_ids);
+        offs = std::max(offs, w.cap_off);
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(w.d_ids[i]);
+            cudaFree(w.d_off[i]);
+            w.d_ids[i] = nullptr;
+            w.d_off[i] = nullptr;
+            if (w.h_ids[i]) cudaFreeHost(w.h_ids[i]);
+            if (w.h_off[i]) cudaFreeHost(w.h_off[i]);
+            w.h_ids[i] = nullptr;
+            w.h_off[i] = nullptr;
+        }
+        for (int i = 0; i < 2; ++i) {
+            ARE_CUDA(cudaMalloc(&w.d_ids[i], (ids + 4) * sizeof(uint32_t)));
+            ARE_CUDA(cudaMalloc(&w.d_off[i], offs * sizeof(int64_t)));
+            if (bounce) {
+                ARE_CUDA(cudaHostAlloc(&w.h_ids[i], (ids + 4) * sizeof(uint32_t), cudaHostAllocDefault));
+                ARE_CUDA(cudaHostAlloc(&w.h_off[i], offs * sizeof(int64_t), cudaHostAllocDefault));
+            }
+        }
+        w.cap_ids = ids;
+        w.cap_off = offs;
+    }
+    if (outs > w.cap_out) {
+        cudaFree(w.d_out);
+        w.d_out = nullptr;
+        ARE_CUDA(cudaMalloc(&w.d_out, outs * sizeof(double)));
+        w.cap_out = outs;
+    }
+    return ARE_OK;
+}
+
+static bool is_pinned(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Exactness precondition of the hot-set kernel (DESIGN.md "Zero-skip
+// exactness"): a zero table entry must contribute +-0 through the financial
+// terms.  Evaluated in the reference's float64 arithmetic.
+static bool fin_zero_ok(const Fin &f) {
+    for (double z : {0.0, -0.0}) {
+        double l = f.rate * z - f.ret;
+        if (l < 0.0) l = 0.0;
+        if (l > f.lim) l = f.lim;
+        const double v = f.share * l;
+        if (!(v == 0.0)) return false;
+    }
+    return true;
+}
+static bool occ_zero_ok(double occ_ret, double occ_lim) {
+    double o = 0.0 - occ_ret;
+    if (o < 0.0) o = 0.0;
+    if (o > occ_lim) o = occ_lim;
+    return o == 0.0;
+}
+
+static int choose_variant(const are_plan_s *p, double occ_ret, double occ_lim, int variant, int *out) {
+    const bool exact = p->zero_skip && occ_zero_ok(occ_ret, occ_lim);
+    if (variant == ARE_VARIANT_AUTO) {
+        *out = exact ? ARE_VARIANT_HOTSET : ARE_VARIANT_DENSE;
+        return ARE_OK;
+    }
+    if (variant == ARE_VARIANT_HOTSET && !exact)
+        return fail(ARE_EINVAL, "hot-set kernel requested but a zero loss does not map to zero under these terms");
+    if (variant != ARE_VARIANT_HOTSET && variant != ARE_VARIANT_DENSE) return fail(ARE_EINVAL, "unknown K2 variant");
+    *out = variant;
+    return ARE_OK;
+}
+
+static void fill_args(const are_plan_s *p, K2Args &a, double occ_ret, double occ_lim, double agg_ret,
+                      double agg_lim) {
+    a.filter = p->pb.filter;
+    a.filter_words = p->pb.filter_words;
+    a.nbits = (uint32_t)p->nbits;
+    a.hash_mode = p->hash_mode;
+    a.slots = p->pb.slots;
+    a.ovf = p->pb.ovf;
+    a.row_len = (uint32_t)p->tab->row_len;
+    a.fin = p->d_fin;
+    a.n_sel = (int32_t)p->n_sel;
+    a.fin_bytes = (int32_t)(p->n_sel * sizeof(Fin));
+    a.occ_ret = occ_ret;
+    a.occ_lim = occ_lim;
+    a.agg_ret = agg_ret;
+    a.agg_lim = agg_lim;
+    a.stacked = p->tab->d;
+    a.rows = p->d_rows;
+}
+
+}  // namespace are
+
+extern "C" {
+
+const char *are_last_error(void) { return t_err.c_str(); }
+int are_version(void) { return 1; }
+int64_t are_launch_count(void) { return g_launches.load(); }
+
+int are_device_count(int *n) {
+    ARE_CUDA(cudaGetDeviceCount(n));
+    return ARE_OK;
+}
+
+int are_select_device(int ordinal) {
+    DeviceInfo *d;
+    return use_device(ordinal, &d);
+}
+
+int are_device_sm_count(int *n) {
+    int dev;
+    int rc = current_device(&dev);
+    if (rc) return rc;
+    DeviceInfo *d;
+    if ((rc = use_device(dev, &d))) return rc;
+    *n = d->sms;
+    return ARE_OK;
+}
+
+int are_host_register(void *ptr, int64_t bytes) {
+    if (!ptr || bytes <= 0) return ARE_OK;
+    cudaError_t e = cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+        cudaGetLastError();
+        return ARE_OK;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaHostRegister");
+    return ARE_OK;
+}
+
+int are_host_unregister(void *ptr) {
+    cudaError_t e = cudaHostUnregister(ptr);
+    if (e != cudaSuccess && e != cudaErrorHostMemoryNotRegistered) return cuda_fail(e, "cudaHostUnregister");
+    cudaGetLastError();
+    return ARE_OK;
+}
+
+// ---- K1 -------------------------------------------------------------------
+int are_tables_from_dense(const double *stacked, int64_t n_tables, int64_t row_len, are_tables_t *out) {
+    if (n_tables < 0 || row_len < 1 || (n_tables > 0 && !stacked)) return fail(ARE_EINVAL, "bad table shape");
+    if (row_len > 0xFFFFFFFFll) return fail(ARE_EINVAL, "catalog exceeds uint32 event ids");
+    int dev, rc;
+    if ((rc = current_device(&dev))) return rc;
+    DeviceInfo *di;
+    if ((rc = use_device(dev, &di))) return rc;
+    auto *t = new are_tables_s();
+    t->device = dev;
+    t->n_tables = n_tables;
+    t->row_len = row_len;
+    const size_t bytes = (size_t)std::max<int64_t>(n_tables, 1) * row_len * sizeof(double);
+    cudaError_t e = cudaMalloc(&t->d, bytes);
+    if (e != cudaSuccess) {
+        delete t;
+        return cuda_fail(e, "cudaMalloc(tables)");
+    }
+    if (n_tables > 0) e = cudaMemcpy(t->d, stacked, (size_t)n_tables * row_len * sizeof(double), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(t->d);
+        delete t;
+        return cuda_fail(e, "upload tables");
+    }
+    *out = t;
+    return ARE_OK;
+}
+
+int are_tables_from_records(const uint32_t *ids, const double *losses, const int64_t *table_offsets,
+                            int64_t n_tables, int64_t row_len, are_tables_t *out) {
+    if (n_tables < 0 || row_len < 1 || !table_offsets) return fail(ARE_EINVAL, "bad table shape");
+    if (row_len > 0xFFFFFFFFll) return fail(ARE_EINVAL, "catalog exceeds uint32 event ids");
+    const int64_t total = table_offsets[n_tables];
+    int64_t max_rec = 0;
+    for (int64_t i = 0; i < n_tables; ++i) {
+        const int64_t lo = table_offsets[i], hi = table_offsets[i + 1];
+        if (hi < lo) return fail(ARE_EINVAL, "table offsets must be non-decreasing");
+        max_rec = std::max(max_rec, hi - lo);
+        for (int64_t r = lo; r < hi; ++r)
+            if (ids[r] < 1 || (int64_t)ids[r] >= row_len)
+                return fail(ARE_ERANGE, "elt[" + std::to_string(i) + "] holds event ids outside [1, " +
+                                            std::to_string(row_len - 1) + "]");
+    }
+    int dev, rc;
+    if ((rc = current_device(&dev))) return rc;
+    DeviceInfo *di;
+    if ((rc = use_device(dev, &di))) return rc;
+    auto *t = new are_tables_s();
+    t->device = dev;
+    t->n_tables = n_tables;
+    t->row_len = row_len;
+    uint32_t *d_ids = nullptr;
+    double *d_loss = nullptr;
+    int64_t *d_toff = nullptr;
+    cudaStream_t st = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(d_ids);
+        cudaFree(d_loss);
+        cudaFree(d_toff);
+        if (st) cudaStreamDestroy(st);
+    };
+    const size_t bytes = (size_t)std::max<int64_t>(n_tables, 1) * row_len * sizeof(double);
+    cudaError_t e;
+    if ((e = cudaMalloc(&t->d, bytes)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaMalloc(&d_ids, std::max<int64_t>(total, 1) * sizeof(uint32_t))) != cudaSuccess ||
+        (e = cudaMalloc(&d_loss, std::max<int64_t>(total, 1) * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&d_toff, (n_tables + 1) * sizeof(int64_t))) != cudaSuccess) {
+        cleanup();
+        cudaFree(t->d);
+        delete t;
+        return cuda_fail(e, "allocate table build buffers");
+    }
+    cudaMemsetAsync(t->d, 0, bytes, st);
+    if (total) {
+        cudaMemcpyAsync(d_ids, ids, total * sizeof(uint32_t), cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(d_loss, losses, total * sizeof(double), cudaMemcpyHostToDevice, st);
+    }
+    cudaMemcpyAsync(d_toff, table_offsets, (n_tables + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    rc = k1_scatter(d_ids, d_loss, d_toff, n_tables, max_rec, row_len, t->d, di->sms, st);
+    if (rc == ARE_OK) {
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "table scatter");
+    }
+    cleanup();
+    if (rc) {
+        cudaFree(t->d);
+        delete t;
+        return rc;
+    }
+    *out = t;
+    return ARE_OK;
+}
+
+int are_tables_info(are_tables_t t, int64_t *n_tables, int64_t *row_len, int64_t *device_bytes) {
+    if (!t) return fail(ARE_EINVAL, "null tables handle");
+    if (n_tables) *n_tables = t->n_tables;
+    if (row_len) *row_len = t->row_len;
+    if (device_bytes) *device_bytes = std::max<int64_t>(t->n_tables, 1) * t->row_len * (int64_t)sizeof(double);
+    return ARE_OK;
+}
+
+int are_tables_read_row(are_tables_t t, int64_t row, double *host_out) {
+    if (!t) return fail(ARE_EINVAL, "null tables handle");
+    if (row < 0 || row >= t->n_tables) return fail(ARE_EINDEX, "table row out of range");
+    ARE_CUDA(cudaSetDevice(t->device));
+    ARE_CUDA(cudaMemcpy(host_out, t->d + row * t->row_len, t->row_len * sizeof(double), cudaMemcpyDeviceToHost));
+    return ARE_OK;
+}
+
+int are_tables_free(are_tables_t t) {
+    tables_release(t);
+    return ARE_OK;
+}
+
+// ---- plan -------------------------------------------------------------------
+int are_plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
+                   const double *fin_ret, const double *fin_lim, const double *fin_share, are_plan_t *out) {
+    if (!t) return fail(ARE_EINVAL, "null tables handle");
+    if (n_sel < 1) return fail(ARE_EINVAL, "table selection is empty");
+    if (n_sel > ARE_MAX_TABLES)
+        return fail(ARE_EINVAL, "kernel supports at most 256 tables per layer, got " + std::to_string(n_sel));
+    for (int64_t s = 0; s < n_sel; ++s)
+        if (rows[s] < 0 || rows[s] >= t->n_tables) return fail(ARE_EINDEX, "table selection out of range");
+    DeviceInfo *di;
+    int rc;
+    if ((rc = use_device(t->device, &di))) return rc;
+    auto *p = new are_plan_s();
+    p->device = t->device;
+    p->tab = t;
+    t->refs.fetch_add(1);
+    p->n_sel = n_sel;
+    std::vector<Fin> hf(n_sel);
+    p->zero_skip = true;
+    for (int64_t s = 0; s < n_sel; ++s) {
+        hf[s] = Fin{fin_rate[s], fin_ret[s], fin_lim[s], fin_share[s]};
+        p->zero_skip = p->zero_skip && fin_zero_ok(hf[s]);
+    }
+    // filter size: whatever shared memory the hot-set kernel leaves free
+    const int64_t fixed = (int64_t)k2_hotset_fixed_smem((int)n_sel);
+    int64_t avail = std::min<int64_t>(di->smem_optin, k2_max_dynamic_smem()) - fixed - 64;
+    int64_t max_bits = (avail / 16) * 128;
+    int64_t want = ((t->row_len + 127) / 128) * 128;
+    p->nbits = std::min(want, max_bits);
+    if (p->nbits < 128) p->nbits = 128;
+    p->hash_mode = p->nbits >= t->row_len ? 0 : (t->row_len <= 2 * p->nbits ? 1 : 2);
+    p->smem = (size_t)fixed + (size_t)(p->nbits / 8);
+    cudaStream_t st = nullptr;
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaMalloc(&p->d_rows, n_sel * sizeof(int64_t))) != cudaSuccess ||
+        (e = cudaMalloc(&p->d_fin, n_sel * sizeof(Fin))) != cudaSuccess ||
+        (e = cudaMalloc(&p->d_err, sizeof(unsigned int))) != cudaSuccess) {
+        if (st) cudaStreamDestroy(st);
+        are_plan_free(p);
+        return cuda_fail(e, "allocate plan");
+    }
+    cudaMemcpyAsync(p->d_rows, rows, n_sel * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(p->d_fin, hf.data(), n_sel * sizeof(Fin), cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(p->d_err, 0, sizeof(unsigned int), st);
+    rc = k1_build_plan(t->d, t->row_len, p->d_rows, (int)n_sel, p->nbits, p->pb, di->sms, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (rc) {
+        are_plan_free(p);
+        return rc;
+    }
+    *out = p;
+    return ARE_OK;
+}
+
+int are_plan_info(are_plan_t p, are_plan_info_t *info) {
+    if (!p || !info) return fail(ARE_EINVAL, "null plan handle");
+    info->n_sel = p->n_sel;
+    info->row_len = p->tab->row_len;
+    info->hot_events = p->pb.hot_events;
+    info->entries = p->pb.entries;
+    info->overflow_entries = p->pb.overflow_entries;
+    info->filter_bits = p->nbits;
+    info->device_bytes = p->tab->row_len * (int64_t)sizeof(Slot) + p->pb.overflow_entries * (int64_t)sizeof(Entry) +
+                         (p->pb.filter_words + 4) * 4 + p->n_sel * (int64_t)(sizeof(Fin) + sizeof(int64_t));
+    info->zero_skip_exact = p->zero_skip ? 1 : 0;
+    info->smem_bytes = (int32_t)p->smem;
+    return ARE_OK;
+}
+
+int are_plan_free(are_plan_t p) {
+    if (!p) return ARE_OK;
+    cudaSetDevice(p->device);
+    cudaFree(p->d_rows);
+    cudaFree(p->d_fin);
+    cudaFree(p->d_err);
+    cudaFree(p->pb.slots);
+    cudaFree(p->pb.ovf);
+    cudaFree(p->pb.filter);
+    tables_release(p->tab);
+    delete p;
+    return ARE_OK;
+}
+
+// ---- K2 -------------------------------------------------------------------
+int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ, const int64_t *d_offsets,
+                        int64_t n_trials, int64_t first, int64_t last, double occ_ret, double occ_lim,
+                        double agg_ret, double agg_lim, double *d_out, void *stream, int32_t variant) {
+    if (!p) return fail(ARE_EINVAL, "null plan handle");
+    if (first < 0 || last < first || last > n_trials) return fail(ARE_EINVAL, "trial range out of bounds");
+    int v, rc;
+    if ((rc = choose_variant(p, occ_ret, occ_lim, variant, &v))) return rc;
+    DeviceInfo *di;
+    if ((rc = use_device(p->device, &di))) return rc;
+    K2Args a{};
+    a.ids = d_event_ids;
+    a.id_base = 0;
+    a.n_ids = n_occ;
+    a.offsets = d_offsets;
+    a.t_base = 0;
+    a.first = first;
+    a.last = last;
+    a.out = d_out;
+    a.out_base = 0;
+    a.err = p->d_err;
+    fill_args(p, a, occ_ret, occ_lim, agg_ret, agg_lim);
+    return k2_launch(a, v, di->sms, p->smem, (cudaStream_t)stream);
+}
+
+int are_check_errors(are_plan_t p, void *stream) {
+    if (!p) return fail(ARE_EINVAL, "null plan handle");
+    ARE_CUDA(cudaSetDevice(p->device));
+    unsigned int h = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    ARE_CUDA(cudaMemcpyAsync(&h, p->d_err, sizeof(h), cudaMemcpyDeviceToHost, st));
+    ARE_CUDA(cudaStreamSynchronize(st));
+    if (h) {
+        ARE_CUDA(cudaMemsetAsync(p->d_err, 0, sizeof(unsigned int), st));
+        ARE_CUDA(cudaStreamSynchronize(st));
+        return fail(ARE_ERANGE, "event id outside the catalog in the year event table");
+    }
+    return ARE_OK;
+}
+
+int are_simulate_host(are_plan_t p, const uint32_t *event_ids, int64_t n_occ, const int64_t *offsets,
+                      int64_t n_trials, int64_t first, int64_t last, double occ_ret, double occ_lim,
+                      double agg_ret, double agg_lim, double *out, int64_t *lookups, int32_t variant) {
+    if (!p) return fail(ARE_EINVAL, "null plan handle");
+    if (first < 0 || last < first || last > n_trials) return fail(ARE_EINVAL, "trial range out of bounds");
+    if (offsets[n_trials] > n_occ) return fail(ARE_EINVAL, "offsets exceed the occurrence count");
+    int v, rc;
+    if ((rc = choose_variant(p, occ_ret, occ_lim, variant, &v))) return rc;
+    if (lookups) *lookups = p->n_sel * (offsets[last] - offsets[first]);
+    if (last == first) return ARE_OK;
+    DeviceInfo *di;
+    if ((rc = use_device(p->device, &di))) return rc;
+    Workspace &w = g_ws[p->device];
+    std::lock_guard<std::mutex> guard(w.mu);
+
+    // trial chunks of <= CHUNK_OCC occurrences (at least one trial each)
+    std::vector<int64_t> cuts{first};
+    int64_t max_ids = 0, max_offs = 0;
+    while (cuts.back() < last) {
+        const int64_t ta = cuts.back();
+        const int64_t limit = offsets[ta] + CHUNK_OCC;
+        int64_t tb = std::upper_bound(offsets + ta + 1, offsets + last + 1, limit) - offsets - 1;
+        if (tb <= ta) tb = ta + 1;
+        cuts.push_back(tb);
+        max_ids = std::max<int64_t>(max_ids, offsets[tb] - (offsets[ta] & ~(int64_t)3));
+        max_offs = std::max(max_offs, tb - ta + 1);
+    }
+    const bool pinned = is_pinned(event_ids) && is_pinned(offsets);
+    if ((rc = ws_reserve(w, max_ids, max_offs, last - first, !pinned))) return rc;
+    ARE_CUDA(cudaMemsetAsync(w.d_err, 0, sizeof(unsigned int), w.comp));
+    ARE_CUDA(cudaEventRecord(w.consumed[0], w.comp));
+    ARE_CUDA(cudaEventRecord(w.consumed[1], w.comp));
+
+    K2Args a{};
+    fill_args(p, a, occ_ret, occ_lim, agg_ret, agg_lim);
+    a.out = w.d_out;
+    a.out_base = first;
+    a.err = w.d_err;
+    const size_t nchunks = cuts.size() - 1;
+    for (size_t c = 0; c < nchunks; ++c) {
+        const int b = (int)(c & 1);
+        const int64_t ta = cuts[c], tb = cuts[c + 1];
+        const int64_t oa = offsets[ta] & ~(int64_t)3, ob = offsets[tb];
+        const int64_t nid = ob - oa, noff = tb - ta + 1;
+        ARE_CUDA(cudaStreamWaitEvent(w.copy, w.consumed[b], 0));
+        if (pinned) {
+            ARE_CUDA(cudaMemcpyAsync(w.d_ids[b], event_ids + oa, nid * sizeof(uint32_t), cudaMemcpyHostToDevice, w.copy));
+            ARE_CUDA(cudaMemcpyAsync(w.d_off[b], offsets + ta, noff * sizeof(int64_t), cudaMemcpyHostToDevice, w.copy));
+        } else {
+            // the bounce buffer b is free once the copy that last used it finished
+            ARE_CUDA(cudaEventSynchronize(w.copied[b]));
+            std::memcpy(w.h_ids[b], event_ids + oa, nid * sizeof(uint32_t));
+            std::memcpy(w.h_off[b], offsets + ta, noff * sizeof(int64_t));
+            ARE_CUDA(cudaMemcpyAsync(w.d_ids[b], w.h_ids[b], nid * sizeof(uint32_t), cudaMemcpyHostToDevice, w.copy));
+            ARE_CUDA(cudaMemcpyAsync(w.d_off[b], w.h_off[b], noff * sizeof(int64_t), cudaMemcpyHostToDevice, w.copy));
+        }
+        ARE_CUDA(cudaEventRecord(w.copied[b], w.copy));
+        ARE_CUDA(cudaStreamWaitEvent(w.comp, w.copied[b], 0));
+        a.ids = w.d_ids[b];
+        a.id_base = oa;
+        a.n_ids = nid;
+        a.offsets = w.d_off[b];
+        a.t_base = ta;
+        a.first = ta;
+        a.last = tb;
+        if ((rc = k2_launch(a, v, di->sms, p->smem, w.comp))) return rc;
+        ARE_CUDA(cudaEventRecord(w.consumed[b], w.comp));
+    }
+    unsigned int herr = 0;
+    ARE_CUDA(cudaMemcpyAsync(&herr, w.d_err, sizeof(herr), cudaMemcpyDeviceToHost, w.comp));
+    ARE_CUDA(cudaMemcpyAsync(out + first, w.d_out, (last - first) * sizeof(double), cudaMemcpyDeviceToHost, w.comp));
+    ARE_CUDA(cudaStreamSynchronize(w.comp));
+    ARE_CUDA(cudaStreamSynchronize(w.copy));
+    if (herr) return fail(ARE_ERANGE, "event id outside the catalog in the year event table");
+    return ARE_OK;
+}
+
+int are_run_trials(const uint32_t *event_ids, int64_t n_occ, const int64_t *offsets, int64_t n_offsets,
+                   const double *stacked, int64_t n_tables, int64_t row_len, const int64_t *rows, int64_t n_sel,
+                   const double *fin_rate, const double *fin_ret, const double *fin_lim, const double *fin_share,
+                   double occ_ret, double occ_lim, double agg_ret, double agg_lim, int64_t chunk,
+                   int64_t first_trial, int64_t last_trial, double *out, int64_t scratch_len, int64_t *lookups) {
+    if (n_sel > ARE_MAX_TABLES)
+        return fail(ARE_EINVAL, "kernel supports at most 256 tables per layer, got " + std::to_string(n_sel));
+    if (chunk > 0 && scratch_len < chunk) return fail(ARE_EINVAL, "scratch smaller than chunk size");
+    if (n_offsets < 1) return fail(ARE_EINVAL, "offsets must hold at least one boundary");
+    if (lookups) *lookups = 0;
+    if (last_trial <= first_trial) return ARE_OK;
+    are_tables_t t = nullptr;
+    are_plan_t p = nullptr;
+    int rc = are_tables_from_dense(stacked, n_tables, row_len, &t);
+    if (rc) return rc;
+    rc = are_plan_build(t, rows, n_sel, fin_rate, fin_ret, fin_lim, fin_share, &p);
+    if (rc == ARE_OK)
+        rc = are_simulate_host(p, event_ids, n_occ, offsets, n_offsets - 1, first_trial, last_trial, occ_ret,
+                               occ_lim, agg_ret, agg_lim, out, lookups, ARE_VARIANT_AUTO);
+    are_plan_free(p);
+    are_tables_free(t);
+    return rc;
+}
+
+// ---- K3 -------------------------------------------------------------------
+int are_order_stats_device(const double *d_losses, int64_t n, const double *rps, int64_t n_rp, double *pml_out,
+                           double *tvar_out, void *stream) {
+    int dev, rc;
+    if ((rc = current_device(&dev))) return rc;
+    DeviceInfo *di;
+    if ((rc = use_device(dev, &di))) return rc;
+    return k3_order_stats(d_losses, n, rps, n_rp, pml_out, tvar_out, di->sms, (cudaStream_t)stream);
+}
+
+int are_order_stats_host(const double *losses, int64_t n, const double *rps, int64_t n_rp, double *pml_out,
+                         double *tvar_out) {
+    if (n <= 0) return fail(ARE_EINVAL, "empty year loss table");
+    int dev, rc;
+    if ((rc = current_device(&dev))) return rc;
+    DeviceInfo *di;
+    if ((rc = use_device(dev, &di))) return rc;
+    cudaStream_t st;
+    ARE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    double *d = nullptr;
+    cudaError_t e = cudaMallocAsync(&d, n * sizeof(double), st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d, losses, n * sizeof(double), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+        cudaStreamDestroy(st);
+        return cuda_fail(e, "upload year loss table");
+    }
+    rc = k3_order_stats(d, n, rps, n_rp, pml_out, tvar_out, di->sms, st);
+    cudaFreeAsync(d, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    return rc;
+}
+
+int are_rollup_device(const double *const *d_ylts, int64_t n_layers, int64_t n, double *d_out, void *stream) {
+    int dev, rc;
+    if ((rc = current_device(&dev))) return rc;
+    DeviceInfo *di;
+    if ((rc = use_device(dev, &di))) return rc;
+    return k3_rollup_launch(d_ylts, n_layers, n, d_out, di->sms, (cudaStream_t)stream);
+}
+
+}  // extern "C"

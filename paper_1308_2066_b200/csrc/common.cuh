@@ -1,0 +1,129 @@
+// Shared definitions for the aggrisk B200 library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "aggrisk_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "paper_1308_2066_b200 is written for sm_100a (B200) only"
+#endif
+
+namespace are {
+
+// ---- error plumbing -----------------------------------------------------
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+extern std::atomic<int64_t> g_launches;
+
+#define ARE_CUDA(call)                                                       \
+    do {                                                                     \
+        cudaError_t _e = (call);                                             \
+        if (_e != cudaSuccess) return ::are::cuda_fail(_e, #call);           \
+    } while (0)
+
+#define ARE_LAUNCHED()                                                       \
+    do {                                                                     \
+        ::are::g_launches.fetch_add(1, std::memory_order_relaxed);           \
+        cudaError_t _e = cudaGetLastError();                                 \
+        if (_e != cudaSuccess) return ::are::cuda_fail(_e, "kernel launch"); \
+    } while (0)
+
+// ---- device-side data layout ------------
+// One 16-byte record per catalog slot (event id).  `meta` packs the
+// selection position of the first non-zero loss (bits 0..15) and the number
+// of non-zero losses n (bits 16..31; n == 0 means absent from every selected
+// table).  Losses 2..n live in the overflow array at `ovf`.
+struct __align__(16) Slot {
+    double x;       // first non-zero loss (float64, exact copy of the table)
+    uint32_t meta;  // j0 | n << 16
+    uint32_t ovf;   // offset of entries 2..n in the overflow array
+};
+
+struct __align__(16) Entry {
+    double x;
+    uint32_t j;     // selection position
+    uint32_t pad;
+};
+
+// Financial terms of one selected table (FinancialTerms, model.py:46-66).
+struct __align__(32) Fin {
+    double rate, ret, lim, share;
+};
+
+// Reference arithmetic, no contraction (pkg/setup.py:9 -ffp-contract=off):
+// every product and sum rounds separately, and clamps are two `if`s so NaN
+// passes through (_kernel.pyx:72-75, :79-82, :114-117).
+__device__ __forceinline__ double clamp_ref(double v, double hi) {
+    if (v < 0.0) v = 0.0;
+    if (v > hi) v = hi;
+    return v;
+}
+__device__ __forceinline__ double fin_term(const Fin &f, double x) {
+    double l = __dsub_rn(__dmul_rn(f.rate, x), f.ret);
+    return __dmul_rn(f.share, clamp_ref(l, f.lim));
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Streaming 16-byte load for the YET id stream: read once, keep it out of L1
+// and mark it evict-first in L2 so it does not displace the hot-set records.
+__device__ __forceinline__ uint4 ld_stream_u4(const uint32_t *p, uint64_t policy) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(policy));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *p, uint64_t policy) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(r) : "l"(p), "l"(policy));
+    return r;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// Hot-set record load: 16 B, L2 evict-last (the records are the L2-resident
+// working set; K2).
+__device__ __forceinline__ Slot ld_slot(const Slot *p, uint64_t policy) {
+    uint4 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(policy));
+    Slot s;
+    s.x = __hiloint2double((int)r.y, (int)r.x);
+    s.meta = r.z;
+    s.ovf = r.w;
+    return s;
+}
+
+// Order-preserving map float64 -> uint64 (NaN sorts last, as numpy does).
+__device__ __forceinline__ uint64_t order_key(double v) {
+    if (v != v) return 0xFFFFFFFFFFFFFFFFull;
+    uint64_t b = (uint64_t)__double_as_longlong(v);
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_value(uint64_t k) {
+    if (k == 0xFFFFFFFFFFFFFFFFull) return __longlong_as_double(0x7FF8000000000000ll);
+    uint64_t b = (k & 0x8000000000000000ull) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+    return __longlong_as_double((long long)b);
+}
+
+}  // namespace are

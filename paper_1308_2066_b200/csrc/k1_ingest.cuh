@@ -1,0 +1,26 @@
+#pragma once
+#include "common.cuh"
+
+namespace are {
+
+struct PlanBuffers {
+    Slot *slots = nullptr;       // row_len records
+    Entry *ovf = nullptr;        // overflow entries
+    uint32_t *filter = nullptr;  // filter_words (+4 pad) words
+    int64_t filter_words = 0;
+    int64_t hot_events = 0;
+    int64_t entries = 0;
+    int64_t overflow_entries = 0;
+};
+
+int k1_scatter(const uint32_t *d_ids, const double *d_losses, const int64_t *d_table_offsets,
+               int64_t n_tables, int64_t max_records, int64_t row_len, double *d_stacked,
+               int sms, cudaStream_t st);
+
+int k1_build_plan(const double *d_stacked, int64_t row_len, const int64_t *d_rows, int n_sel,
+                  int64_t filter_bits, PlanBuffers &pb, int sms, cudaStream_t st);
+
+int scan_exclusive_u32(const uint32_t *d_in, uint32_t *d_out, int64_t n, uint64_t *d_tiles,
+                       uint64_t *h_total, cudaStream_t st);
+
+}  // namespace are

@@ -1,0 +1,43 @@
+#pragma once
+#include "common.cuh"
+
+namespace are {
+
+// Arguments of one K2 launch.  Indices are absolute (reference numbering):
+// occurrence i lives at ids[i - id_base], trial t's offsets at
+// offsets[t - t_base], and its result goes to out[t - out_base].
+struct K2Args {
+    const uint32_t *ids;
+    int64_t id_base;
+    int64_t n_ids;
+    const int64_t *offsets;
+    int64_t t_base;
+    int64_t first, last;
+    double *out;
+    int64_t out_base;
+    // hot set
+    const uint32_t *filter;
+    int64_t filter_words;  // multiple of 4
+    uint32_t nbits;
+    int32_t hash_mode;     // 0: e, 1: e - nbits once, 2: e % nbits
+    const Slot *slots;
+    const Entry *ovf;
+    uint32_t row_len;
+    // terms
+    const Fin *fin;
+    int32_t n_sel;
+    int32_t fin_bytes;     // n_sel * sizeof(Fin)
+    double occ_ret, occ_lim, agg_ret, agg_lim;
+    // dense variant
+    const double *stacked;
+    const int64_t *rows;
+    unsigned int *err;
+};
+
+// Largest dynamic shared-memory carve-out requested by K2 (sm_100: 227 KB).
+inline int k2_max_dynamic_smem() { return 227 * 1024; }
+size_t k2_hotset_fixed_smem(int n_sel);
+int k2_prepare(int device);
+int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStream_t st);
+
+}  // namespace are

@@ -1,0 +1,12 @@
+#pragma once
+#include "common.cuh"
+
+namespace are {
+
+int order_stat_k(int64_t n, double rp, int64_t *k);
+int k3_order_stats(const double *d_x, int64_t n, const double *rps, int64_t n_rp, double *pml_out,
+                   double *tvar_out, int sms, cudaStream_t st);
+int k3_rollup_launch(const double *const *d_ylts_host_array, int64_t n_layers, int64_t n, double *d_out,
+                     int sms, cudaStream_t st);
+
+}  // namespace are

@@ -1,0 +1,319 @@
+"""Aggregate-analysis entry points on the B200 engine.
+
+Mirrors the reference engine API (pkg/src/aggrisk/engine/__init__.py):
+`EngineConfig`, `RunStats`, `run_aggregate_analysis[_with_stats]`,
+`run_chunked`, `price_layer`, `analyse_trial`, the scalar term helpers, and
+the backend plug-in function `run_trials` with the exact argument list of the
+reference's compiled kernel (_kernel.pyx:17-30).  Every simulation runs in
+`libaggrisk_b200.so` (K1/K2 on the GPU); there is no CPU path.
+
+Backend naming: the reference accepts {"auto", "compiled", "python"}
+(__init__.py:60-70) and its suite pins that "cuda" is rejected
+(test_engine.py:229).  This engine's backend is "b200"; "auto" resolves to it.
+"""
+
+from __future__ import annotations
+
+import time
+import weakref
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _native
+from .direct_access import DirectAccessTable, TableSet, memory_footprint
+from .errors import EventOutOfRangeError, PortfolioInvalidError
+from .portfolio import FinancialTerms, Layer, LayerTerms, Trial, YearLossTable, validate_portfolio
+
+UNCHUNKED = None
+DEFAULT_CHUNK_SIZE = 4
+BACKEND = "b200"
+DEFAULT_BACKEND = BACKEND
+HAVE_COMPILED = True  # the engine is always native; absence of the .so raises on use
+
+
+def resolve_backend(name: str = "auto") -> str:
+    if name in ("auto", BACKEND):
+        return BACKEND
+    raise ValueError(f"unknown backend {name!r} (this engine provides {BACKEND!r})")
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    """Execution knobs (reference __init__.py:73-89).
+
+    `worker_count` and `chunk_size` keep their reference validation; the
+    GPU result does not depend on them (the reference guarantees bit-identity
+    across both, test_engine.py:93-103, and so does this engine).
+    `variant` selects the K2 kernel: "auto" (hot-set when exact, else
+    dense), "hotset" or "dense".
+    """
+
+    worker_count: int = 1
+    chunk_size: int | None = DEFAULT_CHUNK_SIZE
+    deterministic: bool = True
+    backend: str = "auto"
+    variant: str = "auto"
+
+    def __post_init__(self):
+        if self.worker_count < 1:
+            raise ValueError("worker_count must be >= 1")
+        if self.chunk_size is not None and self.chunk_size < 1:
+            raise ValueError("chunk_size must be >= 1 or None for unchunked")
+        if not self.deterministic:
+            raise ValueError("nondeterministic execution is not supported")
+        resolve_backend(self.backend)
+        if self.variant not in _native.VARIANTS:
+            raise ValueError(f"unknown kernel variant {self.variant!r}")
+
+
+@dataclass
+class RunStats:
+    """Counters and timings of one run (reference __init__.py:92-106)."""
+
+    trials: int = 0
+    layers: int = 0
+    lookups: int = 0
+    sim_seconds: float = 0.0
+    build_seconds: float = 0.0
+    peak_table_bytes: int = 0
+
+    @property
+    def trials_per_sec(self) -> float:
+        done = self.trials * self.layers
+        return done / self.sim_seconds if self.sim_seconds > 0 else float("inf")
+
+
+# ---------------------------------------------------------- term helpers --
+# Scalar restatements of the three term stages (reference __init__.py:109-144);
+# they document the semantics and are used by tests, not on the GPU path.
+
+def apply_financial_terms(loss: float, terms: FinancialTerms) -> float:
+    v = min(max(terms.exchange_rate * loss - terms.event_retention, 0.0), terms.event_limit)
+    res = terms.share * v
+    assert res >= 0.0
+    return res
+
+
+def apply_occurrence_terms(loss: float, terms: LayerTerms) -> float:
+    res = min(max(loss - terms.occ_retention, 0.0), terms.occ_limit)
+    assert res >= 0.0
+    return res
+
+
+def apply_aggregate_terms(occ_losses: Sequence[float], terms: LayerTerms) -> float:
+    """Cumulative form: prefix sums, clamp, difference, sum; equals the
+    telescoped closed form min(max(total - aggR, 0), aggL) (asserted)."""
+    x = np.asarray(occ_losses, dtype=np.float64)
+    if x.size == 0:
+        return 0.0
+    run = np.add.accumulate(x)
+    cl = np.minimum(np.maximum(run - terms.agg_retention, 0.0), terms.agg_limit)
+    steps = np.diff(cl, prepend=0.0)
+    res = float(np.add.accumulate(steps)[-1])
+    if __debug__:
+        closed = min(max(float(run[-1]) - terms.agg_retention, 0.0), terms.agg_limit)
+        assert abs(res - closed) <= 1e-9 * max(1.0, abs(closed))
+    return res
+
+
+# ------------------------------------------------------------- partition --
+
+def split_by_events(offsets: np.ndarray, parts: int) -> list[tuple[int, int]]:
+    """Contiguous trial ranges with balanced occurrence counts.
+
+    Bit-exact restatement of the reference `_split_by_events`
+    (engine/__init__.py:151-159): targets round(total*k/parts) with Python's
+    round-half-even, left searchsorted, de-duplicated bounds.  It is the
+    trial -> GPU partition of the multi-GPU path.
+    """
+    n = int(offsets.shape[0]) - 1
+    parts = max(1, min(int(parts), n))
+    total = int(offsets[-1])
+    targets = [round(total * k / parts) for k in range(1, parts)]
+    cuts = np.searchsorted(offsets, targets, side="left").tolist()
+    bounds = sorted({0, n, *(int(c) for c in cuts)})
+    return [(a, b) for a, b in zip(bounds[:-1], bounds[1:]) if a < b]
+
+
+_split_by_events = split_by_events  # reference spelling
+
+
+# ------------------------------------------------------------ the plug-in --
+
+# device tables cached per caller-owned `stacked` array (immutable inputs,
+# reference model.py:186-187 / tables.py:84); evicted when the array dies
+_dense_cache: dict[int, tuple] = {}
+
+
+def _tables_for(stacked: np.ndarray):
+    key = id(stacked)
+    hit = _dense_cache.get(key)
+    if hit is not None and hit[0]() is stacked:
+        return hit[1]
+    holder = _DenseTables(stacked)
+    try:
+        ref = weakref.ref(stacked, lambda _r, k=key: _dense_cache.pop(k, None))
+    except TypeError:  # not weak-referenceable: no caching
+        return holder
+    _dense_cache[key] = (ref, holder)
+    return holder
+
+
+class _DenseTables:
+    """Device copy of a caller's dense `stacked` array plus its plans."""
+
+    def __init__(self, stacked: np.ndarray):
+        self.dev = _native.tables_from_dense(stacked)
+        self.plans: dict = {}
+
+    def plan(self, rows, rate, ret, lim, share):
+        key = tuple(np.asarray(a).tobytes() for a in (rows, rate, ret, lim, share))
+        p = self.plans.get(key)
+        if p is None:
+            if len(self.plans) >= 8:
+                self.plans.pop(next(iter(self.plans))).close()
+            p = self.plans[key] = _native.plan_build(self.dev, rows, rate, ret, lim, share)
+        return p
+
+
+def _need(a, dtype, name: str, ndim: int = 1) -> np.ndarray:
+    # the reference's typed memoryviews reject wrong dtypes / non-contiguous
+    # buffers with ValueError (_kernel.pyx:17-30); so do we
+    if not isinstance(a, np.ndarray) or a.dtype != dtype or a.ndim != ndim or not a.flags.c_contiguous:
+        raise ValueError(f"{name}: expected a C-contiguous {np.dtype(dtype).name} array of {ndim} dim(s)")
+    return a
+
+
+def run_trials(event_ids, offsets, stacked, rows, fin_rate, fin_ret, fin_lim, fin_share,
+               occ_ret, occ_lim, agg_ret, agg_lim, chunk, first_trial, last_trial, out, scratch=None,
+               variant: str = "auto") -> int:
+    """Backend plug-in: same arguments and return value as the reference
+    `run_trials` (_kernel.pyx:17-119); simulates trials [first, last) on the
+    GPU and writes out[first:last].  Returns n_sel * occurrences."""
+    ids = _need(event_ids, np.uint32, "event_ids")
+    offs = _need(offsets, np.int64, "offsets")
+    stk = _need(stacked, np.float64, "stacked", 2)
+    rows = _need(rows, np.int64, "rows")
+    fins = [_need(a, np.float64, n) for a, n in
+            ((fin_rate, "fin_rate"), (fin_ret, "fin_ret"), (fin_lim, "fin_lim"), (fin_share, "fin_share"))]
+    res = _need(out, np.float64, "out")
+    if rows.shape[0] > 256:
+        raise ValueError(f"kernel supports at most 256 tables per layer, got {rows.shape[0]}")
+    if chunk > 0:
+        slen = len(scratch) if scratch is not None and hasattr(scratch, "__len__") else (
+            scratch.combined.shape[0] if scratch is not None else 0)
+        if slen < chunk:
+            raise ValueError("scratch smaller than chunk size")
+    if not 0 <= first_trial <= last_trial <= offs.shape[0] - 1:
+        raise ValueError("trial range out of bounds")
+    if last_trial == first_trial:
+        return 0
+    plan = _tables_for(stk).plan(rows, *fins)
+    lookups = _native._I64()
+    _native.check(_native.load().are_simulate_host(
+        plan.value, ids.ctypes.data, ids.shape[0], offs.ctypes.data, offs.shape[0] - 1,
+        int(first_trial), int(last_trial), float(occ_ret), float(occ_lim), float(agg_ret), float(agg_lim),
+        res.ctypes.data, _native.ctypes.byref(lookups), _native.VARIANTS[variant]))
+    return int(lookups.value)
+
+
+# -------------------------------------------------------------- the layer --
+
+def _simulate(yet, tset: TableSet, selection, terms: LayerTerms, cfg: EngineConfig, out: np.ndarray) -> int:
+    rows, rate, ret, lim, share = tset.selection_arrays(selection)
+    n = int(yet.offsets.shape[0]) - 1
+    if n == 0:
+        return 0
+    plan = tset.plan(rows, rate, ret, lim, share)
+    resident = getattr(yet, "_device", None)
+    if resident is not None:  # DeviceYearEventTable: ids already in HBM
+        return resident.simulate(plan, rows.shape[0], terms, out, cfg.variant)
+    ids = np.ascontiguousarray(yet.event_ids, dtype=np.uint32)
+    offs = np.ascontiguousarray(yet.offsets, dtype=np.int64)
+    lookups = _native._I64()
+    _native.check(_native.load().are_simulate_host(
+        plan.value, ids.ctypes.data, ids.shape[0], offs.ctypes.data, n, 0, n,
+        float(terms.occ_retention), float(terms.occ_limit), float(terms.agg_retention),
+        float(terms.agg_limit), out.ctypes.data, _native.ctypes.byref(lookups),
+        _native.VARIANTS[cfg.variant]))
+    return int(lookups.value)
+
+
+def price_layer(yet, tset: TableSet, selection: Sequence[int] | None, terms: LayerTerms,
+                cfg: EngineConfig | None = None, pool=None) -> tuple[np.ndarray, int]:
+    """Interactive path (reference __init__.py:204-221): prebuilt tables, ad-hoc
+    terms and selection, no validation, no table rebuild."""
+    cfg = cfg or EngineConfig()
+    out = np.empty(int(yet.offsets.shape[0]) - 1, dtype=np.float64)
+    return out, _simulate(yet, tset, selection, terms, cfg, out)
+
+
+def run_aggregate_analysis_with_stats(layers: Sequence[Layer], yet, cfg: EngineConfig | None = None,
+                                      pool=None) -> tuple[list[YearLossTable], RunStats]:
+    """Validate, then per layer: K1 build (build_seconds), K2 (sim_seconds)."""
+    cfg = cfg or EngineConfig()
+    violations = validate_portfolio(layers, yet)
+    if violations:
+        raise PortfolioInvalidError(violations)
+    stats = RunStats(trials=int(yet.offsets.shape[0]) - 1, layers=len(layers))
+    ylts: list[YearLossTable] = []
+    for layer in layers:
+        t0 = time.perf_counter()
+        tset = TableSet.from_elts(layer.elts, yet.catalog_size)
+        stats.build_seconds += time.perf_counter() - t0
+        stats.peak_table_bytes = max(stats.peak_table_bytes, memory_footprint(tset.tables).total_bytes)
+        t0 = time.perf_counter()
+        out = np.empty(stats.trials, dtype=np.float64)
+        stats.lookups += _simulate(yet, tset, None, layer.terms, cfg, out)
+        stats.sim_seconds += time.perf_counter() - t0
+        ylts.append(YearLossTable(layer.id, out))
+    return ylts, stats
+
+
+def run_aggregate_analysis(layers: Sequence[Layer], yet, cfg: EngineConfig | None = None) -> list[YearLossTable]:
+    return run_aggregate_analysis_with_stats(layers, yet, cfg)[0]
+
+
+def run_chunked(layers: Sequence[Layer], yet, cfg: EngineConfig | None = None) -> list[YearLossTable]:
+    cfg = cfg or EngineConfig()
+    if cfg.chunk_size is None:
+        raise ValueError("run_chunked requires cfg.chunk_size")
+    return run_aggregate_analysis(layers, yet, cfg)
+
+
+def analyse_trial(trial: Trial, layer: Layer, tables=None, cfg: EngineConfig | None = None) -> float:
+    """Net loss of one trial under one layer (reference __init__.py:278-320)."""
+    cfg = cfg or EngineConfig()
+    if tables is None:
+        tset = TableSet.from_elts(layer.elts)
+    elif isinstance(tables, TableSet):
+        tset = tables
+    else:
+        tset = TableSet.from_tables(list(tables))
+    if len(tset) != len(layer.elts):
+        raise ValueError("tables not aligned with layer elts")
+    ids = np.ascontiguousarray(trial.event_ids, dtype=np.uint32)
+    if ids.size and (int(ids.min()) < 1 or int(ids.max()) > tset.catalog_size):
+        bad = ids[(ids < 1) | (ids > tset.catalog_size)][0]
+        raise EventOutOfRangeError(f"event {int(bad)} outside catalog 1..{tset.catalog_size}")
+    offs = np.array([0, ids.size], dtype=np.int64)
+    out = np.zeros(1, dtype=np.float64)
+    rows, rate, ret, lim, share = tset.selection_arrays(None)
+    plan = tset.plan(rows, rate, ret, lim, share)
+    t = layer.terms
+    lookups = _native._I64()
+    _native.check(_native.load().are_simulate_host(
+        plan.value, ids.ctypes.data, ids.size, offs.ctypes.data, 1, 0, 1,
+        float(t.occ_retention), float(t.occ_limit), float(t.agg_retention), float(t.agg_limit),
+        out.ctypes.data, _native.ctypes.byref(lookups), _native.VARIANTS[cfg.variant]))
+    return float(out[0])
+
+
+__all__ = [
+    "BACKEND", "DEFAULT_BACKEND", "DEFAULT_CHUNK_SIZE", "HAVE_COMPILED", "UNCHUNKED", "EngineConfig",
+    "RunStats", "analyse_trial", "apply_aggregate_terms", "apply_financial_terms", "apply_occurrence_terms",
+    "price_layer", "resolve_backend", "run_aggregate_analysis", "run_aggregate_analysis_with_stats",
+    "run_chunked", "run_trials", "split_by_events", "DirectAccessTable",
+]

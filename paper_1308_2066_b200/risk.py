@@ -1,0 +1,159 @@
+"""Tail metrics over Year Loss Tables, computed by K3 on the GPU.
+
+Mirrors pkg/src/aggrisk/metrics.py: `pml`, `tvar`, `ep_curve`, `EPCurve`,
+`portfolio_rollup`, with the same rank rule k = n - floor(n / rp)
+(metrics.py:29-42), the same argument errors, and the closed-tail TVaR.
+`order_stats` evaluates many return periods in one device pass (the pricing
+service asks for four at a time, service.py:223-227).
+
+Inputs may be a YearLossTable, a numpy array (copied to the device), or a
+float64 CUDA tensor already in HBM (no copy).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _native
+from .portfolio import YearLossTable
+
+
+def _order_stat_k(n: int, return_period: float) -> int:
+    rp = float(return_period)
+    if not rp > 1.0:
+        raise ValueError(f"return_period must exceed 1, got {return_period}")
+    if rp > n:
+        raise ValueError(f"return_period {return_period} exceeds trial count {n}")
+    return n - math.floor(n / rp)
+
+
+def _is_cuda_tensor(x) -> bool:
+    return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda"))
+
+
+def _source(ylt):
+    losses = ylt.losses if isinstance(ylt, YearLossTable) or hasattr(ylt, "layer_id") else ylt
+    if _is_cuda_tensor(losses):
+        if losses.dim() != 1:
+            raise ValueError("losses must be one-dimensional")
+        return losses.contiguous().double()
+    arr = np.ascontiguousarray(losses, dtype=np.float64)
+    if arr.ndim != 1:
+        raise ValueError("losses must be one-dimensional")
+    return arr
+
+
+def order_stats(ylt, return_periods: Sequence[float], stream=None) -> tuple[np.ndarray, np.ndarray]:
+    """(pml[r], tvar[r]) for every return period, one K3 launch sequence."""
+    src = _source(ylt)
+    n = int(src.shape[0])
+    if n == 0:
+        raise ValueError("empty year loss table")
+    rps = np.ascontiguousarray([float(r) for r in return_periods], dtype=np.float64)
+    for r in rps:
+        _order_stat_k(n, r)
+    pml_out = np.empty(rps.size)
+    tvar_out = np.empty(rps.size)
+    if rps.size == 0:
+        return pml_out, tvar_out
+    lib = _native.load()
+    if _is_cuda_tensor(src):
+        import torch
+
+        st = torch.cuda.current_stream(src.device) if stream is None else stream
+        _native.check(lib.are_order_stats_device(src.data_ptr(), n, rps.ctypes.data, rps.size,
+                                                 pml_out.ctypes.data, tvar_out.ctypes.data,
+                                                 ctypes.c_void_p(st.cuda_stream)))
+    else:
+        _native.check(lib.are_order_stats_host(src.ctypes.data, n, rps.ctypes.data, rps.size,
+                                               pml_out.ctypes.data, tvar_out.ctypes.data))
+    return pml_out, tvar_out
+
+
+def pml(ylt, return_period: float) -> float:
+    """Probable maximum loss at `return_period` (metrics.py:45-52)."""
+    return float(order_stats(ylt, [return_period])[0][0])
+
+
+def tvar(ylt, return_period: float) -> float:
+    """Mean of the losses at and beyond the PML order statistic (metrics.py:55-63)."""
+    return float(order_stats(ylt, [return_period])[1][0])
+
+
+@dataclass(frozen=True)
+class EPCurve:
+    """(loss, exceedance probability) points, probabilities strictly decreasing."""
+
+    points: tuple
+
+    def __post_init__(self):
+        pts = tuple(tuple(p) for p in self.points)
+        object.__setattr__(self, "points", pts)
+        for (l0, p0), (l1, p1) in zip(pts, pts[1:]):
+            if not p1 < p0:
+                raise ValueError("probabilities must be strictly decreasing")
+            if l1 < l0:
+                raise ValueError("losses must be non-decreasing")
+        if any(not 0.0 <= p <= 1.0 for _, p in pts):
+            raise ValueError("probability outside [0, 1]")
+
+    @property
+    def losses(self) -> tuple:
+        return tuple(l for l, _ in self.points)
+
+    @property
+    def probabilities(self) -> tuple:
+        return tuple(p for _, p in self.points)
+
+    def __len__(self) -> int:
+        return len(self.points)
+
+    def __iter__(self):
+        return iter(self.points)
+
+
+def ep_curve(ylt, return_periods: Iterable[float]) -> EPCurve:
+    """PML at each distinct return period, ascending rp (metrics.py:97-115)."""
+    src = _source(ylt)
+    if int(src.shape[0]) == 0:
+        raise ValueError("empty year loss table")
+    rps = sorted({float(r) for r in return_periods})
+    if not rps:
+        raise ValueError("no return periods given")
+    p, _ = order_stats(src, rps)
+    return EPCurve(tuple((float(v), 1.0 / rp) for v, rp in zip(p, rps)))
+
+
+def portfolio_rollup(ylts: Sequence[YearLossTable]) -> YearLossTable:
+    """Per-trial sum across layers in list order (metrics.py:118-133), on the GPU."""
+    if not ylts:
+        raise ValueError("no year loss tables to roll up")
+    if len(ylts) == 1:
+        return ylts[0]
+    n = ylts[0].losses.shape[0]
+    for y in ylts[1:]:
+        if y.losses.shape[0] != n:
+            raise ValueError(f"year loss tables differ in length: {n} vs {y.losses.shape[0]}")
+    import torch
+
+    dev = [torch.as_tensor(np.ascontiguousarray(y.losses, dtype=np.float64)).cuda() for y in ylts]
+    total = rollup_device(dev)
+    return YearLossTable("portfolio", total.cpu().numpy())
+
+
+def rollup_device(tensors, out=None, stream=None):
+    """d_out[t] = ((y0[t] + y1[t]) + ...) for float64 CUDA tensors (K3 roll-up)."""
+    import torch
+
+    n = int(tensors[0].shape[0])
+    out = torch.empty(n, dtype=torch.float64, device=tensors[0].device) if out is None else out
+    ptrs = (ctypes.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+    st = torch.cuda.current_stream(tensors[0].device) if stream is None else stream
+    _native.check(_native.load().are_rollup_device(ctypes.cast(ptrs, ctypes.c_void_p), len(tensors), n, out.data_ptr(),
+                                                   ctypes.c_void_p(st.cuda_stream)))
+    return out

@@ -1,0 +1,88 @@
+"""K3 (device order statistics) against the reference metrics.
+
+PML: exact (an order statistic).  TVaR: rel 1e-12 (the reference's own bound
+against its full-sort oracle, test_metrics.py:44-52) -- the device sums the
+tail in a fixed order with double-double accumulation; numpy sums the
+partitioned tail pairwise.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1308_2066_b200.portfolio import YearLossTable
+from paper_1308_2066_b200.risk import ep_curve, order_stats, pml, portfolio_rollup, tvar
+from tests.conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def _ramp(n=1000):
+    return YearLossTable("ramp", np.arange(1, n + 1, dtype=np.float64))
+
+
+def test_kats(golden):
+    k = golden["kats"]
+    assert pml(_ramp(), 100.0) == k["pml_ramp1000_rp100"] == 990.0
+    assert tvar(_ramp(), 100.0) == k["tvar_ramp1000_rp100"] == 995.0
+    c = ep_curve(_ramp(), [100.0, 2.0, 10.0, 2.0])
+    assert [list(p) for p in c.points] == k["ep_ramp1000"]
+    assert c.probabilities == (0.5, 0.1, 0.01)
+    assert pml(_ramp(10), 10.0) == 9.0 and tvar(_ramp(10), 10.0) == 9.5
+    assert pml(np.arange(10.0, 110.0, 10.0), 3.0) == k["pml_10_110_rp3"] == 70.0
+    flat = YearLossTable("f", np.full(100, 7.5))
+    assert pml(flat, 4.0) == 7.5 and tvar(flat, 4.0) == 7.5
+
+
+def test_argument_errors():
+    with pytest.raises(ValueError):
+        pml(_ramp(100), 1.0)
+    with pytest.raises(ValueError):
+        pml(_ramp(100), 101.0)
+    with pytest.raises(ValueError):
+        pml(np.zeros(0), 2.0)
+    with pytest.raises(ValueError):
+        ep_curve(_ramp(), [])
+
+
+def test_golden_random_ylts():
+    z = np.load(os.path.join(GOLDEN, "metrics_1004.npz"))
+    b = z["bounds"]
+    for i in range(b.size - 1):
+        x = z["losses"][b[i]:b[i + 1]]
+        p, t = order_stats(x, z["rps"][i])
+        assert list(p) == list(z["pml"][i])
+        np.testing.assert_allclose(t, z["tvar"][i], rtol=1e-12)
+        assert np.all(t >= p)
+
+
+def test_large_ylt_with_ties_and_device_input(rng):
+    import torch
+
+    n = 1_000_000
+    x = rng.lognormal(8.0, 1.5, n)
+    x[rng.random(n) < 0.1] = 0.0
+    x[rng.random(n) < 0.1] = 66_000.0  # agg-limit saturation ties, as in C1
+    rps = [1.5, 2.0, 10.0, 50.0, 100.0, 250.0, 1000.0, 10_000.0, float(n)]
+    p, t = order_stats(x, rps)
+    for r, pv, tv in zip(rps, p, t):
+        assert pv == oracle.pml(x, r)
+        assert tv == pytest.approx(oracle.tvar(x, r), rel=1e-12)
+    dp, dt = order_stats(torch.from_numpy(x).cuda(), rps)
+    assert dp.tobytes() == p.tobytes() and dt.tobytes() == t.tobytes()  # deterministic
+
+
+def test_rollup_bitwise(rng):
+    ylts = [YearLossTable(str(i), rng.random(100_003) * 100.0) for i in range(70)]
+    want = ylts[0].losses.copy()
+    for y in ylts[1:]:
+        np.add(want, y.losses, out=want)
+    got = portfolio_rollup(ylts)
+    assert got.layer_id == "portfolio" and got.losses.tobytes() == want.tobytes()
+    assert portfolio_rollup(ylts[:1]) is ylts[0]
+    with pytest.raises(ValueError):
+        portfolio_rollup([])
