@@ -47,6 +47,10 @@ typedef enum {
 #define ARE_VARIANT_AUTO 0   /* hot-set kernel when zero-skip is exact, else dense */
 #define ARE_VARIANT_HOTSET 1 /* force the hot-set kernel (fails if not exact)      */
 #define ARE_VARIANT_DENSE 2  /* force the dense direct-access kernel              */
+/* OR-able flag: the caller guarantees every event id of the YET is < row_len
+ * (validated once, e.g. by validate_portfolio); K2 then skips its per-id
+ * range check.  Without it an out-of-catalog id raises ARE_ERANGE. */
+#define ARE_FLAG_IDS_VALIDATED 0x100
 
 typedef struct are_tables_s *are_tables_t;
 typedef struct are_plan_s *are_plan_t;
@@ -75,6 +79,8 @@ int64_t are_launch_count(void);
  * entry points copy from it without staging. */
 int are_host_register(void *ptr, int64_t bytes);
 int are_host_unregister(void *ptr);
+/* 1 when `ptr` is page-locked host memory the copy engines can read directly. */
+int are_host_is_pinned(const void *ptr);
 
 /* ---- K1: ELT ingestion (replaces TableSet.from_elts, tables.py:95-117) -- */
 /* Dense stacked float64 (n_tables, row_len), row-major, as TableSet.stacked. */

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libaggrisk_
 
 ARE_OK, ARE_EINVAL, ARE_ERANGE, ARE_ECUDA, ARE_ENOMEM, ARE_EINDEX = range(6)
 VARIANTS = {"auto": 0, "hotset": 1, "dense": 2}
+IDS_VALIDATED = 0x100  # ARE_FLAG_IDS_VALIDATED: every YET id is known to be <= catalog
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -50,6 +51,7 @@ SIGNATURES = {
     "are_launch_count": (_I64, []),
     "are_host_register": (ctypes.c_int, [_P, _I64]),
     "are_host_unregister": (ctypes.c_int, [_P]),
+    "are_host_is_pinned": (ctypes.c_int, [_P]),
     "are_tables_from_dense": (ctypes.c_int, [_P, _I64, _I64, ctypes.POINTER(_P)]),
     "are_tables_from_records": (ctypes.c_int, [_P, _P, _P, _I64, _I64, ctypes.POINTER(_P)]),
     "are_tables_info": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),

@@ -86,6 +86,7 @@ struct are_plan_s {
     int64_t nbits = 0;
     int hash_mode = 0;
     bool zero_skip = false;
+    bool slot0_hot = false;
     unsigned int *d_err = nullptr;
     size_t smem = 0;
 };
@@ -191,15 +192,17 @@ static bool occ_zero_ok(double occ_ret, double occ_lim) {
 }
 
 static int choose_variant(const are_plan_s *p, double occ_ret, double occ_lim, int variant, int *out) {
-    const bool exact = p->zero_skip && occ_zero_ok(occ_ret, occ_lim);
+    const int flags = variant & ~0xFF;
+    variant &= 0xFF;
+    const bool exact = p->zero_skip && !p->slot0_hot && occ_zero_ok(occ_ret, occ_lim);
     if (variant == ARE_VARIANT_AUTO) {
-        *out = exact ? ARE_VARIANT_HOTSET : ARE_VARIANT_DENSE;
+        *out = (exact ? ARE_VARIANT_HOTSET : ARE_VARIANT_DENSE) | flags;
         return ARE_OK;
     }
     if (variant == ARE_VARIANT_HOTSET && !exact)
         return fail(ARE_EINVAL, "hot-set kernel requested but a zero loss does not map to zero under these terms");
     if (variant != ARE_VARIANT_HOTSET && variant != ARE_VARIANT_DENSE) return fail(ARE_EINVAL, "unknown K2 variant");
-    *out = variant;
+    *out = variant | flags;
     return ARE_OK;
 }
 
@@ -261,6 +264,8 @@ int are_host_register(void *ptr, int64_t bytes) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaHostRegister");
     return ARE_OK;
 }
+
+int are_host_is_pinned(const void *ptr) { return is_pinned(ptr) ? 1 : 0; }
 
 int are_host_unregister(void *ptr) {
     cudaError_t e = cudaHostUnregister(ptr);
@@ -430,12 +435,22 @@ int are_plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const dou
     cudaMemcpyAsync(p->d_fin, hf.data(), n_sel * sizeof(Fin), cudaMemcpyHostToDevice, st);
     cudaMemsetAsync(p->d_err, 0, sizeof(unsigned int), st);
     rc = k1_build_plan(t->d, t->row_len, p->d_rows, (int)n_sel, p->nbits, p->pb, di->sms, st);
+    Slot slot0{};
+    if (rc == ARE_OK) {
+        cudaError_t ce = cudaMemcpyAsync(&slot0, p->pb.slots, sizeof(Slot), cudaMemcpyDeviceToHost, st);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+        if (ce != cudaSuccess) rc = cuda_fail(ce, "read slot 0");
+    }
     cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
     if (rc) {
         are_plan_free(p);
         return rc;
     }
+    // K2 reads out-of-trial lanes as event 0; that is only a no-op when the
+    // unused slot 0 (tables.py:5-7) holds no loss.  A caller-supplied dense
+    // table with a loss in column 0 is served by the dense kernel instead.
+    p->slot0_hot = (slot0.meta >> 16) != 0;
     *out = p;
     return ARE_OK;
 }
@@ -450,7 +465,7 @@ int are_plan_info(are_plan_t p, are_plan_info_t *info) {
     info->filter_bits = p->nbits;
     info->device_bytes = p->tab->row_len * (int64_t)sizeof(Slot) + p->pb.overflow_entries * (int64_t)sizeof(Entry) +
                          (p->pb.filter_words + 4) * 4 + p->n_sel * (int64_t)(sizeof(Fin) + sizeof(int64_t));
-    info->zero_skip_exact = p->zero_skip ? 1 : 0;
+    info->zero_skip_exact = (p->zero_skip && !p->slot0_hot) ? 1 : 0;
     info->smem_bytes = (int32_t)p->smem;
     return ARE_OK;
 }

@@ -90,6 +90,17 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *p, uint64_t po
                  : "=r"(r) : "l"(p), "l"(policy));
     return r;
 }
+// Predicated streaming load: returns p[0] when rel < len, else 0 (no access).
+__device__ __forceinline__ uint32_t ld_stream_if(const uint32_t *p, uint32_t rel, uint32_t len, uint64_t policy) {
+    uint32_t r = 0;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "setp.lt.u32 q, %1, %2;\n\t"
+        "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%3], %4;\n\t}"
+        : "+r"(r)
+        : "r"(rel), "r"(len), "l"(p), "l"(policy));
+    return r;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

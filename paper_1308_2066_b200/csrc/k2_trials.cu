@@ -31,28 +31,30 @@
 
 namespace are {
 
-static constexpr int QCAP = 256;  // per-warp hot queue (>= 31 + 128)
+static constexpr int QCAP = 128;  // per-warp hot queue: < 32 pending + 2 rows of 32
 
-__device__ __forceinline__ uint32_t hot_hash(uint32_t e, uint32_t nbits, int mode) {
-    if (mode == 0) return e;
-    if (mode == 1) return e >= nbits ? e - nbits : e;
+// Event id -> filter bit.  HASH 0: the filter covers the catalog (exact);
+// 1: catalog <= 2 * nbits, fold once (min picks e - nbits iff e >= nbits,
+// the unsigned subtraction wraps otherwise); 2: general modulo.
+template <int HASH>
+__device__ __forceinline__ uint32_t hot_hash(uint32_t e, uint32_t nbits) {
+    if (HASH == 0) return e;
+    if (HASH == 1) return min(e, e - nbits);
     return e % nbits;
 }
 
-__device__ __forceinline__ uint4 load_ids4(const uint32_t *ids, int64_t j, int64_t n_ids,
-                                           int64_t rlo, int64_t rhi, uint64_t pol) {
-    if (j >= 0 && j + 4 <= n_ids) return ld_stream_u4(ids + j, pol);
-    uint32_t r[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int64_t i = j + k;
-        r[k] = (i >= rlo && i < rhi) ? ld_stream_u32(ids + i, pol) : 0u;
-    }
-    return make_uint4(r[0], r[1], r[2], r[3]);
-}
-
-template <int NW>
-__global__ void __launch_bounds__(NW * 32, 1) k2_hotset(const K2Args a) {
+// Persistent hot-set kernel.  Each warp owns trials first + gw, first + gw +
+// W, ...; a trial's ids are read as 32-id coalesced rows (row k of a 128-id
+// chunk is ids [base + 32k, base + 32k + 32), lane l takes one id), two chunks
+// kept in flight.  Filter hits are appended, in trial order, to the warp's
+// queue; every 32 queued events form one batch: lane i gathers the record of
+// the i-th event, applies the financial and occurrence terms, and the warp
+// folds the 32 occurrence values into c strictly in order.
+// CHECK = false when the caller has validated every id <= catalog (the
+// reference's validate_portfolio, or DeviceYearEventTable's upload check).
+template <int HASH, bool CHECK>
+__global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
+    constexpr int NW = K2_THREADS / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     Fin *s_fin = reinterpret_cast<Fin *>(smem);
     double *s_occ = reinterpret_cast<double *>(smem + a.fin_bytes);
@@ -70,41 +72,40 @@ __global__ void __launch_bounds__(NW * 32, 1) k2_hotset(const K2Args a) {
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double *ob = s_occ + warp * 32;
+    const double2 *ob2 = reinterpret_cast<const double2 *>(ob);
     uint32_t *q = s_q + warp * QCAP;
-    const uint32_t lt = lanemask_lt();
+    const uint32_t lt = (1u << lane) - 1u;
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
+    const uint32_t nbits = a.nbits, last_id = a.row_len - 1;
+    const double occ_ret = a.occ_ret, occ_lim = a.occ_lim;
+    const uint32_t *const ids = a.ids;
     const int64_t W = (int64_t)gridDim.x * NW;
-    bool bad = false;
+    uint32_t emax = 0;  // largest id seen: ids > catalog are reported, not read
 
-    // Process `n` queued hot events (uniform n <= 32), then fold their
-    // occurrence values into c in queue (= trial) order.
-    auto batch = [&](uint32_t qh, uint32_t n, double &c) {
-        if ((uint32_t)lane < n) {
-            const uint32_t e = q[(qh + lane) & (QCAP - 1)];
-            const Slot s = ld_slot(a.slots + e, pol_keep);
-            const uint32_t cnt = s.meta >> 16;
-            double comb = 0.0;
-            if (cnt) {
-                comb = __dadd_rn(0.0, fin_term(s_fin[s.meta & 0xFFFFu], s.x));
-                for (uint32_t i = 1; i < cnt; ++i) {
-                    const Entry en = a.ovf[s.ovf + i - 1];
-                    comb = __dadd_rn(comb, fin_term(s_fin[en.j], en.x));
-                }
-            }
-            ob[lane] = clamp_ref(__dsub_rn(comb, a.occ_ret), a.occ_lim);
+    // Lane's share of one batch: gather the i-th queued event's record, apply
+    // the financial terms in selection order and the occurrence terms.
+    auto occ_of = [&](uint32_t e) -> double {
+        const Slot s = ld_slot(a.slots + e, pol_keep);
+        const uint32_t cnt = s.meta >> 16;
+        double comb = 0.0;
+        if (cnt) comb = __dadd_rn(0.0, fin_term(s_fin[s.meta & 0xFFFFu], s.x));
+#pragma unroll 1
+        for (uint32_t i = 1; i < cnt; ++i) {  // events in several tables (~7%)
+            const Entry en = a.ovf[s.ovf + i - 1];
+            comb = __dadd_rn(comb, fin_term(s_fin[en.j], en.x));
         }
+        return clamp_ref(__dsub_rn(comb, occ_ret), occ_lim);
+    };
+    // Full batch: 32 queued events, then the in-order fold into c.
+    auto batch32 = [&](uint32_t qh, double &c) {
+        ob[lane] = occ_of(q[(qh + lane) & (QCAP - 1)]);
         __syncwarp();
-        if (n == 32) {
-            const double2 *ob2 = reinterpret_cast<const double2 *>(ob);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const double2 p = ob2[i];
-                c = __dadd_rn(c, p.x);
-                c = __dadd_rn(c, p.y);
-            }
-        } else {
-            for (uint32_t i = 0; i < n; ++i) c = __dadd_rn(c, ob[i]);
+        for (int i = 0; i < 16; ++i) {
+            const double2 p = ob2[i];
+            c = __dadd_rn(c, p.x);
+            c = __dadd_rn(c, p.y);
         }
         __syncwarp();
     };
@@ -122,62 +123,71 @@ __global__ void __launch_bounds__(NW * 32, 1) k2_hotset(const K2Args a) {
             nlo = a.offsets[tn - a.t_base];
             nhi = a.offsets[tn - a.t_base + 1];
         }
-        const int64_t rlo = lo - a.id_base, rhi = hi - a.id_base;
-        const int64_t mis = (int64_t)((reinterpret_cast<uintptr_t>(a.ids + rlo) >> 2) & 3);
-        const int64_t start = rlo - mis;
-        const int len = (int)(rhi - rlo);
+        const int64_t rlo = lo - a.id_base;
+        const uint32_t len = (uint32_t)(hi - lo);
+        // rows start on a 128-byte line; `rel` (lane's id index minus the
+        // trial start) wraps for the lanes before the trial, so one unsigned
+        // compare bounds both ends
+        const uint32_t skew = (uint32_t)((reinterpret_cast<uintptr_t>(ids + rlo) >> 2) & 31);
+        const uint32_t *p = ids + (rlo - skew) + lane;
+        uint32_t rel = (uint32_t)lane - skew;
+        const int nchunks = (int)((len + skew + 127) >> 7);
         double c = 0.0;
         uint32_t qh = 0, qt = 0;
 
-        int64_t j = start + 4 * lane;
-        uint4 v = load_ids4(a.ids, j, a.n_ids, rlo, rhi, pol_stream);
-        for (int64_t base = start; base < rhi; base += 128) {
-            uint4 vn = make_uint4(0u, 0u, 0u, 0u);
-            if (base + 128 < rhi) vn = load_ids4(a.ids, j + 128, a.n_ids, rlo, rhi, pol_stream);
+        uint32_t cur[4], nxt[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cur[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nxt[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream);
 
-            const uint32_t ev[4] = {v.x, v.y, v.z, v.w};
-            const int rel = (int)(j - rlo);
-            uint32_t hot = 0;
+        for (int ch = 0; ch < nchunks; ++ch) {
+            uint32_t fut[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if ((unsigned)(rel + k) < (unsigned)len) {
-                    const uint32_t e = ev[k];
-                    if (e >= a.row_len) {
-                        bad = true;
-                    } else {
-                        const uint32_t h = hot_hash(e, a.nbits, a.hash_mode);
-                        hot |= ((s_filter[h >> 5] >> (h & 31)) & 1u) << k;
+            for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 256 + 32 * k, rel + 256 + 32 * k, len, pol_stream);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+#pragma unroll
+                for (int k = 2 * half; k < 2 * half + 2; ++k) {
+                    // out-of-trial lanes read 0: event 0 is never hot (slot 0
+                    // unused; a plan with a loss there runs the dense kernel)
+                    uint32_t e = cur[k];
+                    if (CHECK) {
+                        emax = max(emax, e);
+                        e = min(e, last_id);
                     }
+                    const uint32_t h = hot_hash<HASH>(e, nbits);
+                    const bool hot = (s_filter[h >> 5] >> (h & 31)) & 1u;
+                    const uint32_t b = __ballot_sync(0xffffffffu, hot);
+                    if (hot) q[(qt + __popc(b & lt)) & (QCAP - 1)] = e;
+                    qt += __popc(b);
                 }
-            }
-            // lane-major compaction keeps trial order: lane l's hot events
-            // follow those of lanes < l
-            const uint32_t cnt = __popc(hot);
-            const uint32_t b0 = __ballot_sync(0xffffffffu, cnt & 1u);
-            const uint32_t b1 = __ballot_sync(0xffffffffu, cnt & 2u);
-            const uint32_t b2 = __ballot_sync(0xffffffffu, cnt & 4u);
-            const uint32_t tot = __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
-            if (tot) {
-                uint32_t w = qt + __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if ((hot >> k) & 1u) q[(w++) & (QCAP - 1)] = ev[k];
-                qt += tot;
                 __syncwarp();
                 while (qt - qh >= 32u) {
-                    batch(qh, 32u, c);
+                    batch32(qh, c);
                     qh += 32u;
                 }
             }
-            v = vn;
-            j += 128;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                cur[k] = nxt[k];
+                nxt[k] = fut[k];
+            }
+            p += 128;
+            rel += 128;
         }
-        if (qt != qh) batch(qh, qt - qh, c);
+        const uint32_t n = qt - qh;  // final partial batch
+        if (n) {
+            if ((uint32_t)lane < n) ob[lane] = occ_of(q[(qh + lane) & (QCAP - 1)]);
+            __syncwarp();
+            for (uint32_t i = 0; i < n; ++i) c = __dadd_rn(c, ob[i]);
+            __syncwarp();
+        }
         if (lane == 0) a.out[t - a.out_base] = clamp_ref(__dsub_rn(c, a.agg_ret), a.agg_lim);
         lo = nlo;
         hi = nhi;
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.err, 1u);
+    if (CHECK && __any_sync(0xffffffffu, emax > last_id) && lane == 0) atomicOr(a.err, 1u);
 }
 
 // Literal reference loop: every occurrence, every selected row, in order.
@@ -223,24 +233,34 @@ __global__ void __launch_bounds__(NW * 32) k2_dense(const K2Args a) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.err, 1u);
 }
 
-static constexpr int HOT_WARPS = 16;
 static constexpr int DENSE_WARPS = 8;
 
 size_t k2_hotset_fixed_smem(int n_sel) {
-    return (size_t)n_sel * sizeof(Fin) + (size_t)HOT_WARPS * 32 * sizeof(double) +
-           (size_t)HOT_WARPS * QCAP * sizeof(uint32_t);
+    constexpr int NW = K2_THREADS / 32;
+    return (size_t)n_sel * sizeof(Fin) + (size_t)NW * 32 * sizeof(double) + (size_t)NW * QCAP * sizeof(uint32_t);
+}
+
+template <int HASH, bool CHECK>
+static int prepare_one() {
+    ARE_CUDA(cudaFuncSetAttribute(k2_hotset<HASH, CHECK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  k2_max_dynamic_smem()));
+    return ARE_OK;
 }
 
 int k2_prepare(int device) {
     (void)device;
-    ARE_CUDA(cudaFuncSetAttribute(k2_hotset<HOT_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  k2_max_dynamic_smem()));
+    int rc;
+    if ((rc = prepare_one<0, true>()) || (rc = prepare_one<1, true>()) || (rc = prepare_one<2, true>()) ||
+        (rc = prepare_one<0, false>()) || (rc = prepare_one<1, false>()) || (rc = prepare_one<2, false>()))
+        return rc;
     return ARE_OK;
 }
 
 int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStream_t st) {
     if (a.last <= a.first) return ARE_OK;
     const int64_t trials = a.last - a.first;
+    const bool check = !(variant & ARE_FLAG_IDS_VALIDATED);
+    variant &= 0xFF;
     if (variant == ARE_VARIANT_DENSE) {
         int64_t g = (trials + DENSE_WARPS - 1) / DENSE_WARPS;
         const int64_t cap = (int64_t)sms * 8;
@@ -248,9 +268,19 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
         ARE_LAUNCHED();
         return ARE_OK;
     }
-    int64_t g = (trials + HOT_WARPS - 1) / HOT_WARPS;
+    constexpr int NW = K2_THREADS / 32;
+    int64_t g = (trials + NW - 1) / NW;
     if (g > sms) g = sms;  // persistent: one CTA per SM (the filter fills shared memory)
-    k2_hotset<HOT_WARPS><<<(unsigned)g, HOT_WARPS * 32, smem_bytes, st>>>(a);
+    const dim3 grid((unsigned)g), block(K2_THREADS);
+    const int sel = a.hash_mode * 2 + (check ? 1 : 0);
+    switch (sel) {
+        case 0: k2_hotset<0, false><<<grid, block, smem_bytes, st>>>(a); break;
+        case 1: k2_hotset<0, true><<<grid, block, smem_bytes, st>>>(a); break;
+        case 2: k2_hotset<1, false><<<grid, block, smem_bytes, st>>>(a); break;
+        case 3: k2_hotset<1, true><<<grid, block, smem_bytes, st>>>(a); break;
+        case 4: k2_hotset<2, false><<<grid, block, smem_bytes, st>>>(a); break;
+        default: k2_hotset<2, true><<<grid, block, smem_bytes, st>>>(a); break;
+    }
     ARE_LAUNCHED();
     return ARE_OK;
 }

@@ -34,6 +34,9 @@ struct K2Args {
     unsigned int *err;
 };
 
+// Threads per CTA of the hot-set kernel (one persistent CTA per SM).
+constexpr int K2_THREADS = 1024;
+
 // Largest dynamic shared-memory carve-out requested by K2 (sm_100: 227 KB).
 inline int k2_max_dynamic_smem() { return 227 * 1024; }
 size_t k2_hotset_fixed_smem(int n_sel);

@@ -221,7 +221,10 @@ def run_trials(event_ids, offsets, stacked, rows, fin_rate, fin_ret, fin_lim, fi
 
 # -------------------------------------------------------------- the layer --
 
-def _simulate(yet, tset: TableSet, selection, terms: LayerTerms, cfg: EngineConfig, out: np.ndarray) -> int:
+def _simulate(yet, tset: TableSet, selection, terms: LayerTerms, cfg: EngineConfig, out: np.ndarray,
+              validated: bool = False) -> int:
+    """K2 over every trial of `yet` into `out`; `validated` = the ids were
+    range-checked already (validate_portfolio), so K2 may skip its check."""
     rows, rate, ret, lim, share = tset.selection_arrays(selection)
     n = int(yet.offsets.shape[0]) - 1
     if n == 0:
@@ -230,6 +233,7 @@ def _simulate(yet, tset: TableSet, selection, terms: LayerTerms, cfg: EngineConf
     resident = getattr(yet, "_device", None)
     if resident is not None:  # DeviceYearEventTable: ids already in HBM
         return resident.simulate(plan, rows.shape[0], terms, out, cfg.variant)
+    flags = _native.IDS_VALIDATED if validated else 0
     ids = np.ascontiguousarray(yet.event_ids, dtype=np.uint32)
     offs = np.ascontiguousarray(yet.offsets, dtype=np.int64)
     lookups = _native._I64()
@@ -237,7 +241,7 @@ def _simulate(yet, tset: TableSet, selection, terms: LayerTerms, cfg: EngineConf
         plan.value, ids.ctypes.data, ids.shape[0], offs.ctypes.data, n, 0, n,
         float(terms.occ_retention), float(terms.occ_limit), float(terms.agg_retention),
         float(terms.agg_limit), out.ctypes.data, _native.ctypes.byref(lookups),
-        _native.VARIANTS[cfg.variant]))
+        _native.VARIANTS[cfg.variant] | flags))
     return int(lookups.value)
 
 
@@ -266,7 +270,7 @@ def run_aggregate_analysis_with_stats(layers: Sequence[Layer], yet, cfg: EngineC
         stats.peak_table_bytes = max(stats.peak_table_bytes, memory_footprint(tset.tables).total_bytes)
         t0 = time.perf_counter()
         out = np.empty(stats.trials, dtype=np.float64)
-        stats.lookups += _simulate(yet, tset, None, layer.terms, cfg, out)
+        stats.lookups += _simulate(yet, tset, None, layer.terms, cfg, out, validated=True)
         stats.sim_seconds += time.perf_counter() - t0
         ylts.append(YearLossTable(layer.id, out))
     return ylts, stats

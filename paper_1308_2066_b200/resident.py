@@ -15,6 +15,7 @@ It is accepted by `price_layer` / `run_aggregate_analysis` in place of a host
 from __future__ import annotations
 
 import ctypes
+import warnings
 
 import numpy as np
 
@@ -49,9 +50,23 @@ class DeviceYearEventTable:
         self.offsets = np.ascontiguousarray(yet.offsets, dtype=np.int64)
         self.host = host_yet if host_yet is not None else yet
         ids = np.ascontiguousarray(yet.event_ids, dtype=np.uint32)
-        self.d_ids = torch.from_numpy(ids.view(np.int32)).to(self.device, non_blocking=False)
+        # int32 view of the uint32 ids (torch has no general uint32 math); the
+        # host buffer is only read (copied to HBM), never written
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            self.d_ids = torch.from_numpy(ids.view(np.int32)).to(self.device)
         self.d_offsets = torch.from_numpy(self.offsets).to(self.device)
+        self._check_ids()
         self._device = _Resident(self)
+
+    def _check_ids(self) -> None:
+        """One device pass at upload: are all ids inside [0, catalog]?  Then
+        every later K2 launch over this table skips its per-id range check."""
+        if self.d_ids.numel() == 0:
+            self.ids_validated = True
+            return
+        lo, hi = int(self.d_ids.min()), int(self.d_ids.max())  # ids >= 2^31 view as negative
+        self.ids_validated = lo >= 0 and hi <= self.catalog_size
 
     @classmethod
     def from_device(cls, catalog_size: int, d_ids, d_offsets, host_offsets: np.ndarray):
@@ -62,6 +77,7 @@ class DeviceYearEventTable:
         self.offsets = np.ascontiguousarray(host_offsets, dtype=np.int64)
         self.host = None
         self.d_ids, self.d_offsets = d_ids, d_offsets
+        self._check_ids()
         self._device = _Resident(self)
         return self
 
@@ -94,7 +110,8 @@ class DeviceYearEventTable:
             plan.value, self.d_ids.data_ptr(), int(self.d_ids.numel()), self.d_offsets.data_ptr(), n,
             int(first), int(last), float(terms.occ_retention), float(terms.occ_limit),
             float(terms.agg_retention), float(terms.agg_limit), out.data_ptr(),
-            ctypes.c_void_p(st.cuda_stream), _native.VARIANTS[variant]))
+            ctypes.c_void_p(st.cuda_stream),
+            _native.VARIANTS[variant] | (_native.IDS_VALIDATED if self.ids_validated else 0)))
         if check:
             _native.check(lib.are_check_errors(plan.value, ctypes.c_void_p(st.cuda_stream)))
         return out

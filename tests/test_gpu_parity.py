@@ -299,6 +299,21 @@ def test_long_and_ragged_trials():
         assert got.tobytes() == _oracle_ylt(layer, sub).tobytes()
 
 
+def test_loss_in_unused_slot_zero_is_honoured():
+    """A dense table with a loss in column 0 (the reference reads it for event
+    id 0) routes to the dense kernel and still matches the reference loop."""
+    stacked = np.zeros((2, 11))
+    stacked[0, 0], stacked[0, 4], stacked[1, 9] = 5.0, 100.0, 50.0
+    ids = np.array([4, 0, 9, 0, 4], np.uint32)
+    offs = np.array([0, 2, 5], np.int64)
+    rows = np.arange(2, dtype=np.int64)
+    fin = (np.ones(2), np.zeros(2), np.full(2, np.inf), np.ones(2))
+    got, want = np.empty(2), np.empty(2)
+    run_trials(ids, offs, stacked, rows, *fin, 1.0, 60.0, 0.0, 150.0, 0, 0, 2, got, None)
+    oracle.run_trials_port(ids, offs, stacked, rows, *fin, 1.0, 60.0, 0.0, 150.0, 0, 0, 2, want)
+    assert got.tobytes() == want.tobytes() and want[0] == 60.0 + 4.0
+
+
 def test_event_out_of_range_in_yet_raises():
     layer, _ = _worked()
     yet = YearEventTable(10, np.array([4, 12, 9], np.uint32), None, np.array([0, 3], np.int64))
