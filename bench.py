@@ -129,6 +129,35 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+class GpuLocalCpus:
+    """Temporarily pin this thread to the CPUs NVML reports as local to the
+    GPU, so pinned host buffers are first-touched on the GPU's NUMA node."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.saved = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+            cpus = {w * 64 + b for w, word in enumerate(words) for b in range(64) if word >> b & 1}
+            cpus &= os.sched_getaffinity(0)
+            if cpus:
+                self.saved = os.sched_getaffinity(0)
+                os.sched_setaffinity(0, cpus)
+        except Exception:
+            self.saved = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.saved:
+            os.sched_setaffinity(0, self.saved)
+
+
 # ------------------------------------------------------------------ data --
 
 def make_layer():
@@ -284,8 +313,9 @@ def run_ours(args) -> None:
     value = total_trials * args.steps / (elapsed_ms / 1e3)
 
     # ---- e2e: the public host API on pinned host buffers --------------------
-    pinned = torch.from_numpy(yet.event_ids.view(np.int32)).pin_memory()
-    h_offsets = torch.from_numpy(np.ascontiguousarray(yet.offsets)).pin_memory()
+    with GpuLocalCpus(local):
+        pinned = torch.from_numpy(yet.event_ids.view(np.int32)).pin_memory()
+        h_offsets = torch.from_numpy(np.ascontiguousarray(yet.offsets)).pin_memory()
     hyet = YearEventTable(CATALOG, pinned.numpy().view(np.uint32), None, h_offsets.numpy())
 
     def e2e_step():

@@ -125,6 +125,18 @@ __device__ __forceinline__ Slot ld_slot(const Slot *p, uint64_t policy) {
     return s;
 }
 
+// Predicated 32-bit shared store (keeps queue appends branch-free).
+__device__ __forceinline__ void st_shared_if(uint32_t saddr, uint32_t v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}"
+                 :: "r"(saddr), "r"(v), "r"((uint32_t)pred) : "memory");
+}
+__device__ __forceinline__ uint32_t ballot_full(bool pred) {
+    uint32_t b;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tvote.sync.ballot.b32 %0, q, 0xffffffff;\n\t}"
+                 : "=r"(b) : "r"((uint32_t)pred));
+    return b;
+}
+
 // Order-preserving map float64 -> uint64 (NaN sorts last, as numpy does).
 __device__ __forceinline__ uint64_t order_key(double v) {
     if (v != v) return 0xFFFFFFFFFFFFFFFFull;

@@ -74,7 +74,8 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
     double *ob = s_occ + warp * 32;
     const double2 *ob2 = reinterpret_cast<const double2 *>(ob);
     uint32_t *q = s_q + warp * QCAP;
-    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t q_saddr = (uint32_t)__cvta_generic_to_shared(q);
+    const uint32_t lt = lanemask_lt();
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
     const uint32_t nbits = a.nbits, last_id = a.row_len - 1;
@@ -83,31 +84,39 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
     const int64_t W = (int64_t)gridDim.x * NW;
     uint32_t emax = 0;  // largest id seen: ids > catalog are reported, not read
 
-    // Lane's share of one batch: gather the i-th queued event's record, apply
-    // the financial terms in selection order and the occurrence terms.
-    auto occ_of = [&](uint32_t e) -> double {
-        const Slot s = ld_slot(a.slots + e, pol_keep);
-        const uint32_t cnt = s.meta >> 16;
-        double comb = 0.0;
-        if (cnt) comb = __dadd_rn(0.0, fin_term(s_fin[s.meta & 0xFFFFu], s.x));
+    // A batch is 32 queued events, one per lane.  It runs in two halves so
+    // the record gathers of batch j are in flight while batch j-1 is finished
+    // (terms + in-order fold) and while the next rows are filtered.
+    auto finish = [&](const Slot &s, uint32_t n, double &c) {
+        // lane's event: financial terms in selection order, occurrence terms
+        if ((uint32_t)lane < n) {
+            const uint32_t cnt = s.meta >> 16;
+            double comb = 0.0;
+            if (cnt) comb = __dadd_rn(0.0, fin_term(s_fin[s.meta & 0xFFFFu], s.x));
 #pragma unroll 1
-        for (uint32_t i = 1; i < cnt; ++i) {  // events in several tables (~7%)
-            const Entry en = a.ovf[s.ovf + i - 1];
-            comb = __dadd_rn(comb, fin_term(s_fin[en.j], en.x));
+            for (uint32_t i = 1; i < cnt; ++i) {  // events in several tables (~7%)
+                const Entry en = a.ovf[s.ovf + i - 1];
+                comb = __dadd_rn(comb, fin_term(s_fin[en.j], en.x));
+            }
+            ob[lane] = clamp_ref(__dsub_rn(comb, occ_ret), occ_lim);
         }
-        return clamp_ref(__dsub_rn(comb, occ_ret), occ_lim);
-    };
-    // Full batch: 32 queued events, then the in-order fold into c.
-    auto batch32 = [&](uint32_t qh, double &c) {
-        ob[lane] = occ_of(q[(qh + lane) & (QCAP - 1)]);
         __syncwarp();
+        if (n == 32) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const double2 p = ob2[i];
-            c = __dadd_rn(c, p.x);
-            c = __dadd_rn(c, p.y);
+            for (int i = 0; i < 16; ++i) {
+                const double2 v = ob2[i];
+                c = __dadd_rn(c, v.x);
+                c = __dadd_rn(c, v.y);
+            }
+        } else {
+            for (uint32_t i = 0; i < n; ++i) c = __dadd_rn(c, ob[i]);
         }
         __syncwarp();
+    };
+    auto gather = [&](uint32_t qh, uint32_t n) -> Slot {
+        Slot s{0.0, 0u, 0u};
+        if ((uint32_t)lane < n) s = ld_slot(a.slots + q[(qh + lane) & (QCAP - 1)], pol_keep);
+        return s;
     };
 
     int64_t t = a.first + (int64_t)blockIdx.x * NW + warp;
@@ -134,55 +143,66 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
         const int nchunks = (int)((len + skew + 127) >> 7);
         double c = 0.0;
         uint32_t qh = 0, qt = 0;
+        bool pending = false;  // a gathered, unfinished batch (uniform)
+        Slot ps{0.0, 0u, 0u};
 
-        uint32_t cur[4], nxt[4];
+        // three row buffers rotate by renaming (a register move would wait
+        // for the in-flight load it copies): chunk s+2 loads while s is used
+        uint32_t r0[4], r1[4], r2[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) cur[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream);
+        for (int k = 0; k < 4; ++k) r0[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) nxt[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream);
+        for (int k = 0; k < 4; ++k) r1[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream);
 
-        for (int ch = 0; ch < nchunks; ++ch) {
-            uint32_t fut[4];
+        auto step = [&](uint32_t (&cur)[4], uint32_t (&fut)[4]) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 256 + 32 * k, rel + 256 + 32 * k, len, pol_stream);
+            // filter words for all four rows first (independent shared loads)
+            uint32_t ev[4], word[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                // out-of-trial lanes read 0: event 0 is never hot (slot 0
+                // unused; a plan with a loss there runs the dense kernel)
+                uint32_t e = cur[k];
+                if (CHECK) {
+                    emax = max(emax, e);
+                    e = min(e, last_id);
+                }
+                ev[k] = e;
+                word[k] = s_filter[hot_hash<HASH>(e, nbits) >> 5];
+            }
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
 #pragma unroll
                 for (int k = 2 * half; k < 2 * half + 2; ++k) {
-                    // out-of-trial lanes read 0: event 0 is never hot (slot 0
-                    // unused; a plan with a loss there runs the dense kernel)
-                    uint32_t e = cur[k];
-                    if (CHECK) {
-                        emax = max(emax, e);
-                        e = min(e, last_id);
-                    }
-                    const uint32_t h = hot_hash<HASH>(e, nbits);
-                    const bool hot = (s_filter[h >> 5] >> (h & 31)) & 1u;
-                    const uint32_t b = __ballot_sync(0xffffffffu, hot);
-                    if (hot) q[(qt + __popc(b & lt)) & (QCAP - 1)] = e;
+                    const bool hot = (word[k] >> (hot_hash<HASH>(ev[k], nbits) & 31)) & 1u;
+                    const uint32_t b = ballot_full(hot);
+                    st_shared_if(q_saddr + (((qt + __popc(b & lt)) & (QCAP - 1)) << 2), ev[k], hot);
                     qt += __popc(b);
                 }
                 __syncwarp();
                 while (qt - qh >= 32u) {
-                    batch32(qh, c);
+                    const Slot ns = gather(qh, 32u);
+                    if (pending) finish(ps, 32u, c);
+                    ps = ns;
+                    pending = true;
                     qh += 32u;
                 }
             }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                cur[k] = nxt[k];
-                nxt[k] = fut[k];
-            }
             p += 128;
             rel += 128;
+        };
+        for (int ch = 0; ch < nchunks; ch += 3) {
+            step(r0, r2);
+            if (ch + 1 >= nchunks) break;
+            step(r1, r0);
+            if (ch + 2 >= nchunks) break;
+            step(r2, r1);
         }
         const uint32_t n = qt - qh;  // final partial batch
-        if (n) {
-            if ((uint32_t)lane < n) ob[lane] = occ_of(q[(qh + lane) & (QCAP - 1)]);
-            __syncwarp();
-            for (uint32_t i = 0; i < n; ++i) c = __dadd_rn(c, ob[i]);
-            __syncwarp();
-        }
+        const Slot ns = gather(qh, n);
+        if (pending) finish(ps, 32u, c);
+        if (n) finish(ns, n, c);
         if (lane == 0) a.out[t - a.out_base] = clamp_ref(__dsub_rn(c, a.agg_ret), a.agg_lim);
         lo = nlo;
         hi = nhi;
