@@ -1,0 +1,172 @@
+"""Measurements for the non-headline BASELINE.json configs on one B200.
+
+    python scripts/sweep.py [--quick] [--out profiles/r01_sweep.json]
+
+  C3  1M trials x 1000 events, 16-layer portfolio (seed 2066, 32-ELT pool,
+      15 ELTs per layer; even layers Per-Occurrence XL, odd layers Aggregate
+      XL, terms from the generator), layers run back to back, then the
+      on-device portfolio roll-up and K3 on it.
+  C4  10M trials x 1000 events x 15 ELTs (40 GB of ids generated on the
+      device -- uniform ids, like the reference generator).
+  C5  events/trial E in {100..5000} x ELTs J in {1..64}, T = 1e9 / E trials,
+      catalog 2M: trials/s, K2 ms, algorithmic and compulsory GB/s.
+
+Times are CUDA-event times of the K2 launches (inputs resident in HBM),
+median of 5 after 2 warm-ups.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1308_2066_b200 import _native  # noqa: E402
+from paper_1308_2066_b200.direct_access import TableSet  # noqa: E402
+from paper_1308_2066_b200.portfolio import Layer, LayerTerms  # noqa: E402
+from paper_1308_2066_b200.resident import DeviceYearEventTable  # noqa: E402
+from paper_1308_2066_b200.risk import order_stats, rollup_device  # noqa: E402
+from paper_1308_2066_b200.synth import GeneratorSpec, generate_elt, generate_layer  # noqa: E402
+
+CATALOG = 2_000_000
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+
+
+def device_yet(trials: int, events: int, seed: int) -> DeviceYearEventTable:
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    ids = torch.randint(1, CATALOG + 1, (trials * events + 4,), dtype=torch.int32, device="cuda", generator=g)
+    offsets = np.arange(trials + 1, dtype=np.int64) * events
+    d_off = torch.from_numpy(offsets).cuda()
+    return DeviceYearEventTable.from_device(CATALOG, ids[: trials * events], d_off, offsets)
+
+
+def time_k2(dyet, plan, terms, reps: int = 5, warm: int = 2, variant: str = "auto") -> float:
+    out = torch.empty(dyet.trial_count, dtype=torch.float64, device="cuda")
+    for _ in range(warm):
+        dyet.simulate_device(plan, terms, out=out, variant=variant)
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dyet.simulate_device(plan, terms, out=out, check=False, variant=variant)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def c5(quick: bool) -> list[dict]:
+    spec = GeneratorSpec(seed=2066, catalog_size=CATALOG, elt_count=64, elt_size_range=(10_000, 30_000))
+    pool = [generate_elt(spec, i) for i in range(64)]
+    terms = LayerTerms(500.0, 10_000.0, 140_000.0, 66_000.0)
+    es = [100, 1000, 5000] if quick else [100, 250, 500, 1000, 2000, 5000]
+    js = [1, 15, 64] if quick else [1, 2, 4, 8, 15, 16, 32, 64]
+    rows = []
+    for e in es:
+        t = int(1e9 // e)
+        dyet = device_yet(t, e, seed=e)
+        for j in js:
+            tset = TableSet.from_elts(pool[:j], CATALOG)
+            plan = tset.plan(*tset.selection_arrays(None))
+            info = _native.plan_info(plan)
+            ms = time_k2(dyet, plan, terms)
+            alg = t * (12 + 4 * e * (1 + j))
+            comp = t * (4 * e + 16)
+            rows.append({"events": e, "elts": j, "trials": t, "k2_ms": ms, "trials_per_s": t / (ms / 1e3),
+                         "hot_events": info.hot_events, "entries": info.entries,
+                         "algorithmic_gbs": alg / (ms / 1e3) / 1e9, "algorithmic_frac": alg / (ms / 1e3) / 1e9 / PEAK,
+                         "compulsory_gbs": comp / (ms / 1e3) / 1e9, "compulsory_frac": comp / (ms / 1e3) / 1e9 / PEAK})
+            print(json.dumps(rows[-1]), flush=True)
+            del tset, plan
+        del dyet
+        torch.cuda.empty_cache()
+    return rows
+
+
+def c4(quick: bool) -> dict:
+    trials = 2_000_000 if quick else 10_000_000
+    spec = GeneratorSpec(seed=2066, catalog_size=CATALOG, elt_count=15, elt_size_range=(10_000, 30_000))
+    elts = [generate_elt(spec, i) for i in range(15)]
+    tset = TableSet.from_elts(elts, CATALOG)
+    plan = tset.plan(*tset.selection_arrays(None))
+    dyet = device_yet(trials, 1000, seed=44)
+    terms = LayerTerms(500.0, 10_000.0, 140_000.0, 66_000.0)
+    ms = time_k2(dyet, plan, terms, reps=3)
+    out = {"trials": trials, "events": 1000, "elts": 15, "k2_ms": ms, "trials_per_s": trials / (ms / 1e3),
+           "id_bytes": trials * 4000, "compulsory_frac": trials * 4016 / (ms / 1e3) / 1e9 / PEAK}
+    print(json.dumps(out), flush=True)
+    del dyet
+    torch.cuda.empty_cache()
+    return out
+
+
+def c3(quick: bool) -> dict:
+    trials = 200_000 if quick else 1_000_000
+    spec = GeneratorSpec(seed=2066, catalog_size=CATALOG, elt_count=32, elt_size_range=(10_000, 30_000),
+                         layer_count=16, elts_per_layer=15)
+    pool = [generate_elt(spec, i) for i in range(32)]
+    layers = []
+    for i in range(16):
+        g = generate_layer(spec, i, pool)
+        t = g.terms
+        terms = LayerTerms(t.occ_retention, t.occ_limit, 0.0, math.inf) if i % 2 == 0 else \
+            LayerTerms(0.0, math.inf, t.agg_retention, t.agg_limit)
+        layers.append(Layer(g.id, g.elts, terms))
+    plans = []
+    for lay in layers:
+        ts = TableSet.from_elts(lay.elts, CATALOG)
+        plans.append((ts, ts.plan(*ts.selection_arrays(None))))
+    dyet = device_yet(trials, 1000, seed=33)
+    outs = [torch.empty(trials, dtype=torch.float64, device="cuda") for _ in layers]
+
+    def step():
+        for (ts, plan), lay, o in zip(plans, layers, outs):
+            dyet.simulate_device(plan, lay.terms, out=o, check=False)
+        total = rollup_device(outs)
+        return order_stats(total, [10.0, 50.0, 100.0, 250.0])
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    reps = 3
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        res = step()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    out = {"trials": trials, "layers": 16, "step_ms": ms, "trials_per_s": trials / (ms / 1e3),
+           "layer_trials_per_s": 16 * trials / (ms / 1e3), "portfolio_pml": list(map(float, res[0])),
+           "note": "16 K2 launches (one per layer) + k3_rollup + K3 per step; unfused"}
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.json"))
+    ap.add_argument("--only", default="c3,c4,c5")
+    args = ap.parse_args()
+    res = {"device": torch.cuda.get_device_name(), "peak_hbm_gbs": PEAK, "when": time.strftime("%Y-%m-%dT%H:%M:%SZ")}
+    for name in args.only.split(","):
+        res[name] = globals()[name](args.quick)
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as f:
+        json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
