@@ -146,6 +146,25 @@ int are_run_trials(const uint32_t *event_ids, int64_t n_occ,
                    int64_t chunk, int64_t first_trial, int64_t last_trial,
                    double *out, int64_t scratch_len, int64_t *lookups);
 
+/* ---- K0: YET validation (replaces the YET half of validate_portfolio,
+ * model.py:371-395).  Scans ids [0, n_ids) of d_ids, the n_trials trials of
+ * d_offsets (absolute occurrence indices; trial k of the slice is trial
+ * t_base + k) and, when d_ts is non-null, their timestamps (d_ts[i - ts_base]
+ * is occurrence i).  Slices may be validated piecewise and the reports merged. */
+typedef struct {
+    uint32_t min_id, max_id;   /* over the scanned ids                         */
+    int64_t bad_trials;        /* trials with length outside [1, max_len]      */
+    int64_t first_bad_trial;   /* lowest such trial index, -1 if none          */
+    int64_t unsorted;          /* timestamp drops strictly inside a trial      */
+    int64_t ts_nan;            /* NaN timestamps (numpy min/max propagate NaN) */
+    double ts_min, ts_max;     /* over the non-NaN timestamps                  */
+    int32_t ts_checked;
+} are_yet_report_t;
+int are_validate_yet_device(const uint32_t *d_ids, int64_t n_ids,
+                            const int64_t *d_offsets, int64_t n_trials, int64_t t_base,
+                            const double *d_ts, int64_t ts_base, int64_t max_len,
+                            are_yet_report_t *out, void *stream);
+
 /* ---- K3: order statistics (replaces pml/tvar/ep_curve, metrics.py:29-115) --
  * For each return period rp[r]: k = n - floor(n / rp) (metrics.py:40),
  * pml[r] = k-th smallest loss, tvar[r] = mean of the top n-k+1 losses.

@@ -27,6 +27,20 @@ _I32 = ctypes.c_int32
 _D = ctypes.c_double
 
 
+class YetReport(ctypes.Structure):
+    _fields_ = [
+        ("min_id", ctypes.c_uint32),
+        ("max_id", ctypes.c_uint32),
+        ("bad_trials", _I64),
+        ("first_bad_trial", _I64),
+        ("unsorted", _I64),
+        ("ts_nan", _I64),
+        ("ts_min", _D),
+        ("ts_max", _D),
+        ("ts_checked", _I32),
+    ]
+
+
 class PlanInfo(ctypes.Structure):
     _fields_ = [
         ("n_sel", _I64),
@@ -74,6 +88,8 @@ SIGNATURES = {
         [_P, _I64, _P, _I64, _P, _I64, _I64, _P, _I64, _P, _P, _P, _P,
          _D, _D, _D, _D, _I64, _I64, _I64, _P, _I64, ctypes.POINTER(_I64)],
     ),
+    "are_validate_yet_device": (
+        ctypes.c_int, [_P, _I64, _P, _I64, _I64, _P, _I64, _I64, ctypes.POINTER(YetReport), _P]),
     "are_order_stats_device": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _P]),
     "are_order_stats_host": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P]),
     "are_rollup_device": (ctypes.c_int, [_P, _I64, _I64, _P, _P]),

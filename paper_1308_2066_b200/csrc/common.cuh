@@ -4,7 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
+#include <cstring>
 #include <string>
 
 #include "aggrisk_b200.h"

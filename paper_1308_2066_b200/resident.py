@@ -20,6 +20,7 @@ import warnings
 import numpy as np
 
 from . import _native
+from .portfolio import MAX_TRIAL_LENGTH
 
 
 def _torch():
@@ -41,32 +42,26 @@ class _Resident:
 
 
 class DeviceYearEventTable:
-    """A YET whose ids/offsets live in HBM."""
+    """A YET whose ids/offsets live in HBM (validated on the device, K0)."""
 
     def __init__(self, yet, device: int | None = None, host_yet=None):
         torch = _torch()
-        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
-        self.catalog_size = int(yet.catalog_size)
-        self.offsets = np.ascontiguousarray(yet.offsets, dtype=np.int64)
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self._upload(yet.catalog_size, yet.event_ids, yet.offsets, dev)
         self.host = host_yet if host_yet is not None else yet
-        ids = np.ascontiguousarray(yet.event_ids, dtype=np.uint32)
-        # int32 view of the uint32 ids (torch has no general uint32 math); the
-        # host buffer is only read (copied to HBM), never written
-        with warnings.catch_warnings():
-            warnings.simplefilter("ignore", UserWarning)
-            self.d_ids = torch.from_numpy(ids.view(np.int32)).to(self.device)
-        self.d_offsets = torch.from_numpy(self.offsets).to(self.device)
-        self._check_ids()
-        self._device = _Resident(self)
+        ts = getattr(yet, "timestamps", None)
+        if ts is not None:
+            self.validate_timestamps(ts)
 
-    def _check_ids(self) -> None:
-        """One device pass at upload: are all ids inside [0, catalog]?  Then
-        every later K2 launch over this table skips its per-id range check."""
-        if self.d_ids.numel() == 0:
-            self.ids_validated = True
-            return
-        lo, hi = int(self.d_ids.min()), int(self.d_ids.max())  # ids >= 2^31 view as negative
-        self.ids_validated = lo >= 0 and hi <= self.catalog_size
+    @classmethod
+    def from_host_arrays(cls, catalog_size: int, ids, offsets, device: int | None = None, chunk: int = 1 << 26):
+        """Upload ids (any uint32 array-like, e.g. a memmap) in `chunk`-id pieces."""
+        torch = _torch()
+        self = cls.__new__(cls)
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self._upload(catalog_size, ids, offsets, dev, chunk)
+        self.host = None
+        return self
 
     @classmethod
     def from_device(cls, catalog_size: int, d_ids, d_offsets, host_offsets: np.ndarray):
@@ -77,9 +72,95 @@ class DeviceYearEventTable:
         self.offsets = np.ascontiguousarray(host_offsets, dtype=np.int64)
         self.host = None
         self.d_ids, self.d_offsets = d_ids, d_offsets
-        self._check_ids()
+        self._n_ids = int(d_ids.numel())
+        self._report = None
+        self._validate_ids()
         self._device = _Resident(self)
         return self
+
+    def _upload(self, catalog_size, ids, offsets, dev, chunk: int = 1 << 26) -> None:
+        torch = _torch()
+        self.device = dev
+        self.catalog_size = int(catalog_size)
+        self.offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        n = int(self.offsets[-1])
+        # +4 zero ids of padding: 16-byte loads past the last trial stay in bounds
+        self.d_ids = torch.zeros(n + 4, dtype=torch.int32, device=dev)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            for a in range(0, n, chunk):
+                piece = np.ascontiguousarray(ids[a:min(n, a + chunk)], dtype=np.uint32).view(np.int32)
+                self.d_ids[a:a + piece.shape[0]].copy_(torch.from_numpy(piece))
+        self._n_ids = n
+        self.d_offsets = torch.from_numpy(self.offsets).to(dev)
+        self._report = None
+        self._validate_ids()
+        self._device = _Resident(self)
+
+    # ---- K0 validation ------------------------------------------------------
+    def _k0(self, d_ts=None, ts_base: int = 0, t0: int = 0, t1: int | None = None, ids: bool = True):
+        torch = _torch()
+        t1 = self.trial_count if t1 is None else t1
+        rep = _native.YetReport()
+        st = torch.cuda.current_stream(self.device)
+        _native.check(_native.load().are_validate_yet_device(
+            self.d_ids.data_ptr(), self._n_ids if ids else 0, self.d_offsets.data_ptr() + 8 * t0, t1 - t0, t0,
+            None if d_ts is None else d_ts.data_ptr(), ts_base, MAX_TRIAL_LENGTH, ctypes.byref(rep),
+            ctypes.c_void_p(st.cuda_stream)))
+        return rep
+
+    def _validate_ids(self) -> None:
+        """Ids range + trial lengths, one device pass at upload.  Every later
+        K2 launch over this table then skips its per-id range check."""
+        rep = self._k0()
+        self._report = {"min_id": int(rep.min_id), "max_id": int(rep.max_id), "bad_trials": int(rep.bad_trials),
+                        "first_bad": int(rep.first_bad_trial), "unsorted": 0, "ts_nan": 0,
+                        "ts_min": None, "ts_max": None}
+        self.ids_validated = self._n_ids == 0 or rep.max_id <= self.catalog_size
+
+    def validate_timestamps(self, ts, chunk: int = 1 << 26) -> None:
+        """Stream host timestamps through K0 in trial-aligned chunks (kept nowhere)."""
+        torch = _torch()
+        n_trials = self.trial_count
+        r = self._report
+        t0 = 0
+        while t0 < n_trials:
+            a = int(self.offsets[t0])
+            t1 = int(np.searchsorted(self.offsets, a + chunk, side="right")) - 1
+            t1 = min(max(t1, t0 + 1), n_trials)
+            b = int(self.offsets[t1])
+            d_ts = torch.from_numpy(np.ascontiguousarray(ts[a:b], dtype=np.float64)).to(self.device) if b > a \
+                else torch.zeros(1, dtype=torch.float64, device=self.device)
+            rep = self._k0(d_ts, ts_base=a, t0=t0, t1=t1, ids=False)
+            r["unsorted"] += int(rep.unsorted)
+            r["ts_nan"] += int(rep.ts_nan)
+            if b > a and rep.ts_nan < (b - a):
+                r["ts_min"] = rep.ts_min if r["ts_min"] is None else min(r["ts_min"], rep.ts_min)
+                r["ts_max"] = rep.ts_max if r["ts_max"] is None else max(r["ts_max"], rep.ts_max)
+            t0 = t1
+        r["ts_checked"] = True
+
+    def yet_violations(self):
+        """The YET half of validate_portfolio (model.py:371-395) from K0's counters."""
+        from .portfolio import Violation
+
+        r = self._report
+        out = []
+        if self.trial_count == 0:
+            out.append(Violation("no_trials", "year event table holds no trials"))
+        if r["bad_trials"]:
+            out.append(Violation("trial_length", f"{r['bad_trials']} trial(s) outside [1, {MAX_TRIAL_LENGTH}] "
+                                                 f"occurrences (first: trial {r['first_bad']})"))
+        if self._n_ids:
+            if r["min_id"] < 1 or r["max_id"] > self.catalog_size:
+                out.append(Violation("event_out_of_range", f"trial event id outside [1, {self.catalog_size}]"))
+            # numpy's min/max propagate NaN, and a NaN compares false: no violation
+            if r.get("ts_checked") and not r["ts_nan"] and r["ts_min"] is not None and \
+                    (r["ts_min"] < 0.0 or r["ts_max"] > 1.0):
+                out.append(Violation("bad_timestamp", "timestamps must lie in [0, 1]"))
+            if r["unsorted"]:
+                out.append(Violation("trial_unsorted", f"timestamps decrease inside {r['unsorted']} position(s)"))
+        return out
 
     @property
     def trial_count(self) -> int:
@@ -107,7 +188,7 @@ class DeviceYearEventTable:
         st = torch.cuda.current_stream(self.device) if stream is None else stream
         lib = _native.load()
         _native.check(lib.are_simulate_device(
-            plan.value, self.d_ids.data_ptr(), int(self.d_ids.numel()), self.d_offsets.data_ptr(), n,
+            plan.value, self.d_ids.data_ptr(), self._n_ids, self.d_offsets.data_ptr(), n,
             int(first), int(last), float(terms.occ_retention), float(terms.occ_limit),
             float(terms.agg_retention), float(terms.agg_limit), out.data_ptr(),
             ctypes.c_void_p(st.cuda_stream),

@@ -242,8 +242,23 @@ def c1_fixture():
     return meta, ylt
 
 
+def are1_fixture() -> dict:
+    """A small ARE1 binary YET written by the reference (io.py:150-175)."""
+    from aggrisk.io import save_yet
+
+    spec = GeneratorSpec(seed=5, catalog_size=3_000, trial_count=400,
+                         events_per_trial_range=(0, 60), elt_count=1, elt_size_range=(10, 20))
+    yet = generate_yet(spec)
+    path = os.path.join(HERE, "yet_small.are1")
+    save_yet(yet, path, format="binary")
+    return {"ids_sha256": sha(yet.event_ids), "offsets_sha256": sha(yet.offsets),
+            "timestamps_sha256": sha(yet.timestamps), "catalog": yet.catalog_size,
+            "trials": yet.trial_count}
+
+
 def main() -> None:
     out = {}
+    out["are1"] = are1_fixture()
     out["kats"] = kats()
     out["split_by_events"] = split_cases()
     out["seed31"] = seed31_digest()
