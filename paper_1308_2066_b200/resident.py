@@ -31,6 +31,18 @@ def _torch():
     return torch
 
 
+_UPLOADER = None
+
+
+def _uploader():
+    global _UPLOADER
+    if _UPLOADER is None:
+        from .h2d import Uploader
+
+        _UPLOADER = Uploader()
+    return _UPLOADER
+
+
 class _Resident:
     def __init__(self, owner: "DeviceYearEventTable"):
         self.owner = owner
@@ -86,13 +98,14 @@ class DeviceYearEventTable:
         n = int(self.offsets[-1])
         # +4 zero ids of padding: 16-byte loads past the last trial stay in bounds
         self.d_ids = torch.zeros(n + 4, dtype=torch.int32, device=dev)
-        with warnings.catch_warnings():
-            warnings.simplefilter("ignore", UserWarning)
-            for a in range(0, n, chunk):
-                piece = np.ascontiguousarray(ids[a:min(n, a + chunk)], dtype=np.uint32).view(np.int32)
-                self.d_ids[a:a + piece.shape[0]].copy_(torch.from_numpy(piece))
+        if n:
+            src = ids if getattr(ids, "dtype", None) == np.uint32 else np.asarray(ids, dtype=np.uint32)
+            with torch.cuda.device(dev):
+                _uploader().copy(self.d_ids[:n], src)
         self._n_ids = n
-        self.d_offsets = torch.from_numpy(self.offsets).to(dev)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)  # read-only numpy source
+            self.d_offsets = torch.from_numpy(self.offsets).to(dev)
         self._report = None
         self._validate_ids()
         self._device = _Resident(self)
@@ -129,8 +142,10 @@ class DeviceYearEventTable:
             t1 = int(np.searchsorted(self.offsets, a + chunk, side="right")) - 1
             t1 = min(max(t1, t0 + 1), n_trials)
             b = int(self.offsets[t1])
-            d_ts = torch.from_numpy(np.ascontiguousarray(ts[a:b], dtype=np.float64)).to(self.device) if b > a \
-                else torch.zeros(1, dtype=torch.float64, device=self.device)
+            d_ts = torch.empty(max(b - a, 1), dtype=torch.float64, device=self.device)
+            if b > a:
+                with torch.cuda.device(self.device):
+                    _uploader().copy(d_ts, np.asarray(ts[a:b], dtype=np.float64))
             rep = self._k0(d_ts, ts_base=a, t0=t0, t1=t1, ids=False)
             r["unsorted"] += int(rep.unsorted)
             r["ts_nan"] += int(rep.ts_nan)

@@ -154,6 +154,33 @@ def c3(quick: bool) -> dict:
     return out
 
 
+def validate(quick: bool) -> dict:
+    """validate_portfolio's YET checks on the device (K0,
+    timestamps streamed from the host) vs the host numpy path."""
+    from paper_1308_2066_b200.portfolio import YearEventTable, validate_portfolio
+    from paper_1308_2066_b200.synth import bulk_yet
+
+    trials = 100_000 if quick else 1_000_000
+    yet = bulk_yet(7, CATALOG, 0, trials, 1000, threads=os.cpu_count() or 8)
+    ts = np.tile(np.linspace(0.0, 1.0, 1000), trials)
+    full = YearEventTable(CATALOG, yet.event_ids, ts, yet.offsets)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dyet = DeviceYearEventTable(full)
+    viol = dyet.yet_violations()
+    torch.cuda.synchronize()
+    dev_s = time.perf_counter() - t0
+    sample = full.head(100_000)
+    t0 = time.perf_counter()
+    host_viol = validate_portfolio([], sample)
+    host_s = (time.perf_counter() - t0) * trials / 100_000
+    out = {"trials": trials, "events": 1000, "device_seconds_incl_h2d_of_ids_and_timestamps": dev_s,
+           "host_numpy_seconds_extrapolated_from_100k": host_s, "violations": [str(v) for v in viol],
+           "host_violations_on_sample": [str(v) for v in host_viol]}
+    print(json.dumps(out), flush=True)
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
