@@ -103,6 +103,12 @@ int are_plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel,
                    const double *fin_rate, const double *fin_ret,
                    const double *fin_lim, const double *fin_share,
                    are_plan_t *out);
+/* Plan over an ELT pool for the fused multi-layer kernel (its filter is sized
+ * for that kernel's shared-memory layout).  rows = the pool, in pool order. */
+int are_plan_build_pool(are_tables_t t, const int64_t *rows, int64_t n_sel,
+                        const double *fin_rate, const double *fin_ret,
+                        const double *fin_lim, const double *fin_share,
+                        are_plan_t *out);
 int are_plan_info(are_plan_t p, are_plan_info_t *info);
 int are_plan_free(are_plan_t p);
 
@@ -120,6 +126,20 @@ int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ
                         double occ_ret, double occ_lim, double agg_ret, double agg_lim,
                         double *d_out, void *stream, int32_t variant);
 int are_check_errors(are_plan_t p, void *stream);
+
+/* Fused multi-layer K2 (replaces the per-layer loop of
+ * run_aggregate_analysis_with_stats, engine/__init__.py:242-253).  `p` is a
+ * pool plan (are_plan_build_pool, <= 64 tables); layer l selects the pool rows
+ * in bit mask masks[l] (its selection order must be increasing pool order) and
+ * has terms layer_terms[4l..4l+3] = (occ_ret, occ_lim, agg_ret, agg_lim).
+ * n_layers <= 16.  Writes d_out[l * out_stride + t] for t in [first, last).
+ * Each layer's result is bit-identical to a single-layer run. */
+int are_simulate_layers_device(are_plan_t p, int32_t n_layers, const uint64_t *masks,
+                               const double *layer_terms,
+                               const uint32_t *d_event_ids, int64_t n_occ,
+                               const int64_t *d_offsets, int64_t n_trials,
+                               int64_t first, int64_t last,
+                               double *d_out, int64_t out_stride, void *stream, int32_t flags);
 
 /* Host form: host ids/offsets/out; the library streams trial chunks to the
  * device (overlapping copies with K2) and returns when `out` is filled.

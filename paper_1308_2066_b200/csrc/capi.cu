@@ -87,6 +87,7 @@ struct are_plan_s {
     int hash_mode = 0;
     bool zero_skip = false;
     bool slot0_hot = false;
+    bool pool = false;
     unsigned int *d_err = nullptr;
     size_t smem = 0;
 };
@@ -390,8 +391,9 @@ int are_tables_free(are_tables_t t) {
 }
 
 // ---- plan -------------------------------------------------------------------
-int are_plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
-                   const double *fin_ret, const double *fin_lim, const double *fin_share, are_plan_t *out) {
+static int plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
+                      const double *fin_ret, const double *fin_lim, const double *fin_share, bool pool,
+                      are_plan_t *out) {
     if (!t) return fail(ARE_EINVAL, "null tables handle");
     if (n_sel < 1) return fail(ARE_EINVAL, "table selection is empty");
     if (n_sel > ARE_MAX_TABLES)
@@ -402,6 +404,7 @@ int are_plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const dou
     int rc;
     if ((rc = use_device(t->device, &di))) return rc;
     auto *p = new are_plan_s();
+    p->pool = pool;
     p->device = t->device;
     p->tab = t;
     t->refs.fetch_add(1);
@@ -412,8 +415,10 @@ int are_plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const dou
         hf[s] = Fin{fin_rate[s], fin_ret[s], fin_lim[s], fin_share[s]};
         p->zero_skip = p->zero_skip && fin_zero_ok(hf[s]);
     }
-    // filter size: whatever shared memory the hot-set kernel leaves free
-    const int64_t fixed = (int64_t)k2_hotset_fixed_smem((int)n_sel);
+    if (pool && n_sel > K2L_MAX_POOL)
+        return fail(ARE_EINVAL, "a layer pool holds at most 64 tables, got " + std::to_string(n_sel));
+    // filter size: whatever shared memory the K2 kernel leaves free
+    const int64_t fixed = (int64_t)(pool ? k2_layers_fixed_smem((int)n_sel) : k2_hotset_fixed_smem((int)n_sel));
     int64_t avail = std::min<int64_t>(di->smem_optin, k2_max_dynamic_smem()) - fixed - 64;
     int64_t max_bits = (avail / 16) * 128;
     int64_t want = ((t->row_len + 127) / 128) * 128;
@@ -453,6 +458,16 @@ int are_plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const dou
     p->slot0_hot = (slot0.meta >> 16) != 0;
     *out = p;
     return ARE_OK;
+}
+
+int are_plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
+                   const double *fin_ret, const double *fin_lim, const double *fin_share, are_plan_t *out) {
+    return plan_build(t, rows, n_sel, fin_rate, fin_ret, fin_lim, fin_share, false, out);
+}
+
+int are_plan_build_pool(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
+                        const double *fin_ret, const double *fin_lim, const double *fin_share, are_plan_t *out) {
+    return plan_build(t, rows, n_sel, fin_rate, fin_ret, fin_lim, fin_share, true, out);
 }
 
 int are_plan_info(are_plan_t p, are_plan_info_t *info) {
@@ -507,6 +522,52 @@ int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ
     a.err = p->d_err;
     fill_args(p, a, occ_ret, occ_lim, agg_ret, agg_lim);
     return k2_launch(a, v, di->sms, p->smem, (cudaStream_t)stream);
+}
+
+int are_simulate_layers_device(are_plan_t p, int32_t n_layers, const uint64_t *masks, const double *layer_terms,
+                               const uint32_t *d_event_ids, int64_t n_occ, const int64_t *d_offsets, int64_t n_trials,
+                               int64_t first, int64_t last, double *d_out, int64_t out_stride, void *stream,
+                               int32_t flags) {
+    if (!p) return fail(ARE_EINVAL, "null plan handle");
+    if (!p->pool) return fail(ARE_EINVAL, "the fused layer kernel needs a pool plan (are_plan_build_pool)");
+    if (n_layers < 1 || n_layers > K2L_MAX_LAYERS) return fail(ARE_EINVAL, "1..16 layers per fused launch");
+    if (first < 0 || last < first || last > n_trials) return fail(ARE_EINVAL, "trial range out of bounds");
+    if (!(p->zero_skip && !p->slot0_hot)) return fail(ARE_EINVAL, "pool terms are not zero-exact; run layers singly");
+    const uint64_t valid = p->n_sel >= 64 ? ~0ull : ((1ull << p->n_sel) - 1);
+    std::vector<LayerTerm> lt(n_layers);
+    for (int l = 0; l < n_layers; ++l) {
+        if (masks[l] & ~valid) return fail(ARE_EINDEX, "layer mask names a table outside the pool");
+        lt[l] = LayerTerm{layer_terms[4 * l], layer_terms[4 * l + 1], layer_terms[4 * l + 2], layer_terms[4 * l + 3]};
+        if (!occ_zero_ok(lt[l].occ_ret, lt[l].occ_lim))
+            return fail(ARE_EINVAL, "layer occurrence terms are not zero-exact; run layers singly");
+    }
+    DeviceInfo *di;
+    int rc;
+    if ((rc = use_device(p->device, &di))) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint64_t *d_masks = nullptr;
+    LayerTerm *d_terms = nullptr;
+    ARE_CUDA(cudaMallocAsync((void **)&d_masks, sizeof(uint64_t) * n_layers, st));
+    ARE_CUDA(cudaMallocAsync((void **)&d_terms, sizeof(LayerTerm) * n_layers, st));
+    ARE_CUDA(cudaMemcpyAsync(d_masks, masks, sizeof(uint64_t) * n_layers, cudaMemcpyHostToDevice, st));
+    ARE_CUDA(cudaMemcpyAsync(d_terms, lt.data(), sizeof(LayerTerm) * n_layers, cudaMemcpyHostToDevice, st));
+    K2Args a{};
+    a.ids = d_event_ids;
+    a.id_base = 0;
+    a.n_ids = n_occ;
+    a.offsets = d_offsets;
+    a.t_base = 0;
+    a.first = first;
+    a.last = last;
+    a.out = d_out;
+    a.out_base = 0;
+    a.err = p->d_err;
+    fill_args(p, a, 0.0, 0.0, 0.0, 0.0);
+    K2Layers L{n_layers, out_stride, d_masks, d_terms};
+    rc = k2_layers_launch(a, L, !(flags & ARE_FLAG_IDS_VALIDATED), di->sms, p->smem, st);
+    cudaFreeAsync(d_masks, st);
+    cudaFreeAsync(d_terms, st);
+    return rc;
 }
 
 int are_check_errors(are_plan_t p, void *stream) {

@@ -1,0 +1,273 @@
+// K2-L -- fused multi-layer simulation: one pass over the YET for L layers.
+//
+// SURVEY.md §8(f) row 2.  The reference runs layers as a sequential outer loop
+// (engine/__init__.py:242-253), re-reading the whole event stream per layer.
+// Here a layer set whose ELTs come from one pool of P <= 64 tables shares a
+// single hot-set plan over the pool (selection = the pool in pool order) and a
+// single pass over the ids: the filter flags events present in ANY pool table,
+// and each flagged event is evaluated for every layer.
+//
+// Exactness per layer: layer l's selection must be increasing in pool order
+// (checked on the host), so summing the event's non-zero pool entries that are
+// in l's bitmask, in pool order, is exactly l's `comb` (zero entries add +-0);
+// events absent from l contribute +-0 to l's trial sum; every layer's trial sum
+// is folded strictly in trial order.  So each layer's YLT is bit-identical to
+// running K2 (and the reference) on that layer alone.
+//
+// Work mapping (warp per trial, like k2_hotset): queued events are served in
+// sub-batches of 8.  Lane (i = lane % 8, g = lane / 8) gathers event i's record
+// and evaluates layers g, g+4, g+8, ... for it, writing occ[i][l] to shared
+// memory; then lane l (< L) folds occ[0..n)[l] into its own register c_l.  The
+// fold is therefore lane-parallel across layers instead of warp-redundant.
+#include "k2_trials.cuh"
+
+namespace are {
+
+static constexpr int LQCAP = 128;   // per-warp queue of event ids
+static constexpr int LSUB = 8;      // events per sub-batch
+
+template <int HASH>
+__device__ __forceinline__ uint32_t l_hash(uint32_t e, uint32_t nbits) {
+    if (HASH == 0) return e;
+    if (HASH == 1) return min(e, e - nbits);
+    return e % nbits;
+}
+
+// Evaluate one event (record `s`) for layers sg, sg+4, ... and store each
+// layer's occurrence value at out[l].  Kept out of line: the kernel calls it
+// from several unrolled sites and an inlined copy each would thrash the
+// instruction cache.
+__device__ __noinline__ void layer_eval(const Slot s, const Entry *__restrict__ ovf, const Fin *s_fin,
+                                        const uint64_t *s_mask, const double *s_occ_ret, const double *s_occ_lim,
+                                        int nl, int sg, double *out) {
+    // non-zero pool entries of the event in pool order (first inline, the
+    // rest in the overflow array); financial terms applied once per entry
+    const uint32_t cnt = s.meta >> 16;
+    double f[4];
+    uint32_t jj[4];
+    uint64_t em = 0;  // pool tables the event appears in
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        f[k] = 0.0;
+        jj[k] = 0;
+    }
+    if (cnt) {
+        jj[0] = s.meta & 0xFFFFu;
+        f[0] = fin_term(s_fin[jj[0]], s.x);
+        em = 1ull << jj[0];
+    }
+#pragma unroll 1
+    for (uint32_t k = 1; k < cnt && k < 4; ++k) {
+        const Entry en = ovf[s.ovf + k - 1];
+        jj[k] = en.j;
+        f[k] = fin_term(s_fin[en.j], en.x);
+        em |= 1ull << en.j;
+    }
+#pragma unroll 1
+    for (uint32_t k = 4; k < cnt; ++k) em |= 1ull << ovf[s.ovf + k - 1].j;
+#pragma unroll 1
+    for (int l = sg; l < nl; l += 4) {
+        const uint64_t m = s_mask[l];
+        double o = 0.0;  // layer does not see the event: occ(+0) = +-0, adds nothing
+        if (em & m) {
+            double comb = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if ((uint32_t)k < cnt && ((m >> jj[k]) & 1ull)) comb = __dadd_rn(comb, f[k]);
+#pragma unroll 1
+            for (uint32_t k = 4; k < cnt; ++k) {  // events in > 4 pool tables (rare)
+                const Entry en = ovf[s.ovf + k - 1];
+                if ((m >> en.j) & 1ull) comb = __dadd_rn(comb, fin_term(s_fin[en.j], en.x));
+            }
+            o = clamp_ref(__dsub_rn(comb, s_occ_ret[l]), s_occ_lim[l]);
+        }
+        out[l] = o;
+    }
+}
+
+template <int HASH, bool CHECK>
+__global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, const K2Layers L) {
+    constexpr int NW = K2L_THREADS / 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    Fin *s_fin = reinterpret_cast<Fin *>(smem);
+    uint64_t *s_mask = reinterpret_cast<uint64_t *>(smem + a.fin_bytes);  // per layer
+    double *s_occ_ret = reinterpret_cast<double *>(s_mask + K2L_MAX_LAYERS);
+    double *s_occ_lim = s_occ_ret + K2L_MAX_LAYERS;
+    double *s_occ = s_occ_lim + K2L_MAX_LAYERS;  // [NW][LSUB][K2L_MAX_LAYERS]
+    uint32_t *s_q = reinterpret_cast<uint32_t *>(s_occ + NW * LSUB * K2L_MAX_LAYERS);  // [NW][LQCAP]
+    uint32_t *s_filter = s_q + NW * LQCAP;
+
+    for (int i = threadIdx.x; i < a.n_sel; i += blockDim.x) s_fin[i] = a.fin[i];
+    for (int i = threadIdx.x; i < L.n_layers; i += blockDim.x) {
+        s_mask[i] = L.masks[i];
+        s_occ_ret[i] = L.terms[i].occ_ret;
+        s_occ_lim[i] = L.terms[i].occ_lim;
+    }
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.filter);
+        uint4 *dst = reinterpret_cast<uint4 *>(s_filter);
+        const int n4 = (int)(a.filter_words >> 2);
+        for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int si = lane & (LSUB - 1), sg = lane >> 3;  // sub-batch event, layer group
+    double *occ = s_occ + warp * LSUB * K2L_MAX_LAYERS;  // occ[i * K2L_MAX_LAYERS + l]
+    uint32_t *q = s_q + warp * LQCAP;
+    const uint32_t q_saddr = (uint32_t)__cvta_generic_to_shared(q);
+    const uint32_t lt = lanemask_lt();
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
+    const uint32_t nbits = a.nbits, last_id = a.row_len - 1;
+    const uint32_t *const ids = a.ids;
+    const int64_t W = (int64_t)gridDim.x * NW;
+    const int nl = L.n_layers;
+    // this lane's fold layer (lane < nl)
+    const double agg_ret = lane < nl ? L.terms[lane].agg_ret : 0.0;
+    const double agg_lim = lane < nl ? L.terms[lane].agg_lim : 0.0;
+    uint32_t emax = 0;
+
+    auto gather = [&](uint32_t qh, uint32_t n) -> Slot {
+        Slot s{0.0, 0u, 0u};
+        if ((uint32_t)si < n) s = ld_slot(a.slots + q[(qh + si) & (LQCAP - 1)], pol_keep);
+        return s;
+    };
+    // Evaluate a gathered sub-batch of n <= 8 events and fold it per layer.
+    auto finish = [&](const Slot &s, uint32_t n, double &c) {
+        if ((uint32_t)si < n)
+            layer_eval(s, a.ovf, s_fin, s_mask, s_occ_ret, s_occ_lim, nl, sg, occ + si * K2L_MAX_LAYERS);
+        __syncwarp();
+        if (lane < nl)
+            for (uint32_t i = 0; i < n; ++i) c = __dadd_rn(c, occ[i * K2L_MAX_LAYERS + lane]);
+        __syncwarp();
+    };
+
+    int64_t t = a.first + (int64_t)blockIdx.x * NW + warp;
+    int64_t lo = 0, hi = 0;
+    if (t < a.last) {
+        lo = a.offsets[t - a.t_base];
+        hi = a.offsets[t - a.t_base + 1];
+    }
+    for (; t < a.last; t += W) {
+        const int64_t tn = t + W;
+        int64_t nlo = 0, nhi = 0;
+        if (tn < a.last) {
+            nlo = a.offsets[tn - a.t_base];
+            nhi = a.offsets[tn - a.t_base + 1];
+        }
+        const int64_t rlo = lo - a.id_base;
+        const uint32_t len = (uint32_t)(hi - lo);
+        const uint32_t skew = (uint32_t)((reinterpret_cast<uintptr_t>(ids + rlo) >> 2) & 31);
+        const uint32_t *p = ids + (rlo - skew) + lane;
+        uint32_t rel = (uint32_t)lane - skew;
+        const int nchunks = (int)((len + skew + 127) >> 7);
+        double c = 0.0;  // this lane's layer sum
+        uint32_t qh = 0, qt = 0;
+        bool pending = false;  // a gathered sub-batch not yet evaluated
+        Slot ps{0.0, 0u, 0u};
+
+        uint32_t r0[4], r1[4], r2[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r0[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r1[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream);
+
+        auto step = [&](uint32_t (&cur)[4], uint32_t (&fut)[4]) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 256 + 32 * k, rel + 256 + 32 * k, len, pol_stream);
+            uint32_t ev[4], word[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t e = cur[k];
+                if (CHECK) {
+                    emax = max(emax, e);
+                    e = min(e, last_id);
+                }
+                ev[k] = e;
+                word[k] = s_filter[l_hash<HASH>(e, nbits) >> 5];
+            }
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+#pragma unroll
+                for (int k = 2 * half; k < 2 * half + 2; ++k) {
+                    const bool hot = (word[k] >> (l_hash<HASH>(ev[k], nbits) & 31)) & 1u;
+                    const uint32_t b = ballot_full(hot);
+                    st_shared_if(q_saddr + (((qt + __popc(b & lt)) & (LQCAP - 1)) << 2), ev[k], hot);
+                    qt += __popc(b);
+                }
+                __syncwarp();
+                while (qt - qh >= (uint32_t)LSUB) {
+                    const Slot ns = gather(qh, LSUB);  // in flight while the previous one finishes
+                    if (pending) finish(ps, LSUB, c);
+                    ps = ns;
+                    pending = true;
+                    qh += LSUB;
+                }
+            }
+            p += 128;
+            rel += 128;
+        };
+        for (int ch = 0; ch < nchunks; ch += 3) {
+            step(r0, r2);
+            if (ch + 1 >= nchunks) break;
+            step(r1, r0);
+            if (ch + 2 >= nchunks) break;
+            step(r2, r1);
+        }
+        {
+            const uint32_t n = qt - qh;
+            const Slot ns = gather(qh, n);
+            if (pending) finish(ps, LSUB, c);
+            if (n) finish(ns, n, c);
+        }
+        if (lane < nl) a.out[(int64_t)lane * L.out_stride + (t - a.out_base)] = clamp_ref(__dsub_rn(c, agg_ret), agg_lim);
+        lo = nlo;
+        hi = nhi;
+    }
+    if (CHECK && __any_sync(0xffffffffu, emax > last_id) && lane == 0) atomicOr(a.err, 1u);
+}
+
+size_t k2_layers_fixed_smem(int n_sel) {
+    constexpr int NW = K2L_THREADS / 32;
+    return (size_t)n_sel * sizeof(Fin) + 3 * K2L_MAX_LAYERS * sizeof(double) +
+           (size_t)NW * LSUB * K2L_MAX_LAYERS * sizeof(double) +
+           (size_t)NW * LQCAP * sizeof(uint32_t);
+}
+
+template <int HASH, bool CHECK>
+static int layers_prepare_one() {
+    ARE_CUDA(cudaFuncSetAttribute(k2_layers<HASH, CHECK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  k2_max_dynamic_smem()));
+    return ARE_OK;
+}
+
+int k2_layers_prepare() {
+    int rc;
+    if ((rc = layers_prepare_one<0, true>()) || (rc = layers_prepare_one<1, true>()) ||
+        (rc = layers_prepare_one<2, true>()) || (rc = layers_prepare_one<0, false>()) ||
+        (rc = layers_prepare_one<1, false>()) || (rc = layers_prepare_one<2, false>()))
+        return rc;
+    return ARE_OK;
+}
+
+int k2_layers_launch(const K2Args &a, const K2Layers &L, bool check, int sms, size_t smem_bytes, cudaStream_t st) {
+    if (a.last <= a.first) return ARE_OK;
+    constexpr int NW = K2L_THREADS / 32;
+    const int64_t trials = a.last - a.first;
+    int64_t g = (trials + NW - 1) / NW;
+    if (g > sms) g = sms;
+    const dim3 grid((unsigned)g), block(K2L_THREADS);
+    switch (a.hash_mode * 2 + (check ? 1 : 0)) {
+        case 0: k2_layers<0, false><<<grid, block, smem_bytes, st>>>(a, L); break;
+        case 1: k2_layers<0, true><<<grid, block, smem_bytes, st>>>(a, L); break;
+        case 2: k2_layers<1, false><<<grid, block, smem_bytes, st>>>(a, L); break;
+        case 3: k2_layers<1, true><<<grid, block, smem_bytes, st>>>(a, L); break;
+        case 4: k2_layers<2, false><<<grid, block, smem_bytes, st>>>(a, L); break;
+        default: k2_layers<2, true><<<grid, block, smem_bytes, st>>>(a, L); break;
+    }
+    ARE_LAUNCHED();
+    return ARE_OK;
+}
+
+}  // namespace are

@@ -273,7 +273,7 @@ int k2_prepare(int device) {
     if ((rc = prepare_one<0, true>()) || (rc = prepare_one<1, true>()) || (rc = prepare_one<2, true>()) ||
         (rc = prepare_one<0, false>()) || (rc = prepare_one<1, false>()) || (rc = prepare_one<2, false>()))
         return rc;
-    return ARE_OK;
+    return k2_layers_prepare();
 }
 
 int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStream_t st) {

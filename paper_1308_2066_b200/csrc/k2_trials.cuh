@@ -37,10 +37,29 @@ struct K2Args {
 // Threads per CTA of the hot-set kernel (one persistent CTA per SM).
 constexpr int K2_THREADS = 1024;
 
+// Fused multi-layer kernel (k2_layers.cu): 16 warps per CTA, up to 16 layers
+// per launch over one ELT pool of up to 64 tables.
+constexpr int K2L_THREADS = 512;
+constexpr int K2L_MAX_LAYERS = 16;
+constexpr int K2L_MAX_POOL = 64;
+
+struct LayerTerm {
+    double occ_ret, occ_lim, agg_ret, agg_lim;
+};
+struct K2Layers {
+    int32_t n_layers;
+    int64_t out_stride;      // out[l * out_stride + t]
+    const uint64_t *masks;   // pool-row bitmask per layer
+    const LayerTerm *terms;  // per layer
+};
+
 // Largest dynamic shared-memory carve-out requested by K2 (sm_100: 227 KB).
 inline int k2_max_dynamic_smem() { return 227 * 1024; }
 size_t k2_hotset_fixed_smem(int n_sel);
 int k2_prepare(int device);
 int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStream_t st);
+size_t k2_layers_fixed_smem(int n_sel);
+int k2_layers_prepare();
+int k2_layers_launch(const K2Args &a, const K2Layers &L, bool check, int sms, size_t smem_bytes, cudaStream_t st);
 
 }  // namespace are

@@ -14,6 +14,7 @@ Backend naming: the reference accepts {"auto", "compiled", "python"}
 
 from __future__ import annotations
 
+import math
 import time
 import weakref
 from dataclasses import dataclass
@@ -245,6 +246,96 @@ def _simulate(yet, tset: TableSet, selection, terms: LayerTerms, cfg: EngineConf
     return int(lookups.value)
 
 
+# --------------------------------------------------- fused multi-layer --
+
+MAX_FUSED_LAYERS = 16
+MAX_POOL = 64
+
+
+def layer_pool(layers: Sequence[Layer]):
+    """(pool, masks): one ELT order consistent with every layer's own order,
+    and each layer's selection as a pool bitmask -- or None when the layers
+    cannot share the fused kernel (order conflict, pool > 64 tables)."""
+    pool: list = []
+    index: dict[int, int] = {}
+    succ: dict[int, set] = {}
+    for layer in layers:
+        prev = None
+        for e in layer.elts:
+            k = id(e)
+            if k not in index:
+                index[k] = len(pool)
+                pool.append(e)
+                succ[index[k]] = set()
+            if prev is not None and prev != index[k]:
+                succ[prev].add(index[k])
+            prev = index[k]
+        if len({id(e) for e in layer.elts}) != len(layer.elts):
+            return None  # a table twice in one layer: keep the general path
+    if len(pool) > MAX_POOL:
+        return None
+    indeg = [0] * len(pool)
+    for a, bs in succ.items():
+        for b in bs:
+            indeg[b] += 1
+    order, ready = [], [i for i in range(len(pool)) if indeg[i] == 0]
+    while ready:  # Kahn, lowest first-appearance first
+        ready.sort()
+        i = ready.pop(0)
+        order.append(i)
+        for b in succ[i]:
+            indeg[b] -= 1
+            if indeg[b] == 0:
+                ready.append(b)
+    if len(order) != len(pool):
+        return None  # layers disagree on the relative order of two tables
+    rank = {old: new for new, old in enumerate(order)}
+    masks = [sum(1 << rank[index[id(e)]] for e in layer.elts) for layer in layers]
+    return [pool[i] for i in order], masks
+
+
+def simulate_layers_device(dyet, pool_tset: TableSet, masks, terms_list, out=None, variant_flags: int = 0):
+    """Fused K2 over a DeviceYearEventTable: (L, T) float64 CUDA tensor of YLTs."""
+    import torch
+
+    n = dyet.trial_count
+    L = len(masks)
+    out = torch.empty((L, n), dtype=torch.float64, device=dyet.device) if out is None else out
+    plan = pool_tset.plan(*pool_tset.selection_arrays(None), pool=True)
+    st = torch.cuda.current_stream(dyet.device)
+    lib = _native.load()
+    flags = variant_flags | (_native.IDS_VALIDATED if dyet.ids_validated else 0)
+    for g in range(0, L, MAX_FUSED_LAYERS):
+        m = np.ascontiguousarray(masks[g:g + MAX_FUSED_LAYERS], dtype=np.uint64)
+        lt = np.ascontiguousarray([[t.occ_retention, t.occ_limit, t.agg_retention, t.agg_limit]
+                                   for t in terms_list[g:g + MAX_FUSED_LAYERS]], dtype=np.float64)
+        _native.check(lib.are_simulate_layers_device(
+            plan.value, m.shape[0], m.ctypes.data, lt.ctypes.data, dyet.d_ids.data_ptr(), dyet._n_ids,
+            dyet.d_offsets.data_ptr(), n, 0, n, out[g].data_ptr(), n, _native.ctypes.c_void_p(st.cuda_stream),
+            flags))
+    _native.check(lib.are_check_errors(plan.value, _native.ctypes.c_void_p(st.cuda_stream)))
+    return out
+
+
+def _fusable(layers: Sequence[Layer], cfg: EngineConfig):
+    if len(layers) < 2 or cfg.variant not in ("auto", "hotset"):
+        return None
+    got = layer_pool(layers)
+    if got is None:
+        return None
+    pool, masks = got
+    for e in pool:  # the pool plan must be zero-exact (DESIGN.md §2)
+        t = e.terms
+        if not (t.exchange_rate > 0 and math.isfinite(t.exchange_rate) and t.event_retention >= 0
+                and t.event_limit > 0 and 0 <= t.share <= 1):
+            return None
+    for layer in layers:
+        t = layer.terms
+        if not (t.occ_retention >= 0 and math.isfinite(t.occ_retention) and t.occ_limit >= 0):
+            return None
+    return pool, masks
+
+
 def price_layer(yet, tset: TableSet, selection: Sequence[int] | None, terms: LayerTerms,
                 cfg: EngineConfig | None = None, pool=None) -> tuple[np.ndarray, int]:
     """Interactive path (reference __init__.py:204-221): prebuilt tables, ad-hoc
@@ -263,6 +354,29 @@ def run_aggregate_analysis_with_stats(layers: Sequence[Layer], yet, cfg: EngineC
         raise PortfolioInvalidError(violations)
     stats = RunStats(trials=int(yet.offsets.shape[0]) - 1, layers=len(layers))
     ylts: list[YearLossTable] = []
+    fused = _fusable(layers, cfg)
+    if fused is not None and stats.trials > 0:
+        # one pass over the YET for every layer
+        from .resident import DeviceYearEventTable
+        import torch
+
+        pool, masks = fused
+        t0 = time.perf_counter()
+        tset = TableSet.from_elts(pool, yet.catalog_size)
+        tset.plan(*tset.selection_arrays(None), pool=True)
+        stats.build_seconds += time.perf_counter() - t0
+        stats.peak_table_bytes = memory_footprint(tset.tables).total_bytes
+        dyet = yet if getattr(yet, "_device", None) is not None else DeviceYearEventTable(yet)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d = simulate_layers_device(dyet, tset, masks, [layer.terms for layer in layers])
+        host = d.cpu().numpy()
+        stats.sim_seconds += time.perf_counter() - t0
+        occ = int(yet.offsets[-1])
+        for i, layer in enumerate(layers):
+            stats.lookups += len(layer.elts) * occ
+            ylts.append(YearLossTable(layer.id, host[i]))
+        return ylts, stats
     for layer in layers:
         t0 = time.perf_counter()
         tset = TableSet.from_elts(layer.elts, yet.catalog_size)

@@ -147,9 +147,33 @@ def c3(quick: bool) -> dict:
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps
+    # fused: one pass over the YET for all 16 layers
+    from paper_1308_2066_b200.engine import layer_pool, simulate_layers_device
+
+    pool_elts, masks = layer_pool(layers)
+    ptset = TableSet.from_elts(pool_elts, CATALOG)
+    fused = torch.empty((16, trials), dtype=torch.float64, device="cuda")
+
+    def fused_step():
+        simulate_layers_device(dyet, ptset, masks, [l.terms for l in layers], out=fused)
+        total = rollup_device([fused[i] for i in range(16)])
+        return order_stats(total, [10.0, 50.0, 100.0, 250.0])
+
+    for _ in range(2):
+        fres = fused_step()
+    same = all(torch.equal(fused[i], outs[i]) for i in range(16))
+    a.record()
+    for _ in range(reps):
+        fres = fused_step()
+    b.record()
+    torch.cuda.synchronize()
+    fms = a.elapsed_time(b) / reps
     out = {"trials": trials, "layers": 16, "step_ms": ms, "trials_per_s": trials / (ms / 1e3),
            "layer_trials_per_s": 16 * trials / (ms / 1e3), "portfolio_pml": list(map(float, res[0])),
-           "note": "16 K2 launches (one per layer) + k3_rollup + K3 per step; unfused"}
+           "note": "16 K2 launches (one per layer) + k3_rollup + K3 per step; unfused",
+           "fused_step_ms": fms, "fused_trials_per_s": trials / (fms / 1e3),
+           "fused_layer_trials_per_s": 16 * trials / (fms / 1e3), "fused_bitwise_equal_unfused": bool(same),
+           "fused_portfolio_pml": list(map(float, fres[0]))}
     print(json.dumps(out), flush=True)
     return out
 

@@ -375,3 +375,38 @@ def test_c2_shape_sample_and_partition_invariance():
                                  yet.offsets[a:b + 1] - yet.offsets[a])
             pieces.append(price_layer(sub, tset, None, layer.terms)[0])
         assert np.concatenate(pieces).tobytes() == whole.tobytes()
+
+
+# ------------------------------------------------- fused multi-layer (C3) --
+
+def test_fused_layers_bitwise_equal_single_layer_runs():
+    """one pass for 16 layers == 16 single-layer runs, bitwise."""
+    import math as _m
+
+    from paper_1308_2066_b200.engine import _fusable
+
+    spec = GeneratorSpec(seed=2066, catalog_size=300_000, trial_count=3_000, events_per_trial_range=(200, 1200),
+                         elt_count=32, elt_size_range=(2_000, 8_000), layer_count=16, elts_per_layer=15)
+    yet = generate_yet(spec, ids_only=True)
+    pool = [generate_elt(spec, i) for i in range(32)]
+    from paper_1308_2066_b200.synth import generate_layer as _gl
+
+    layers = []
+    for i in range(16):
+        g = _gl(spec, i, pool)
+        t = g.terms
+        terms = LayerTerms(t.occ_retention, t.occ_limit, 0.0, _m.inf) if i % 2 == 0 else \
+            LayerTerms(0.0, _m.inf, t.agg_retention, t.agg_limit)
+        layers.append(Layer(g.id, g.elts, terms))
+    assert _fusable(layers, EngineConfig()) is not None
+    fused, stats = run_aggregate_analysis_with_stats(layers, yet)
+    assert stats.lookups == sum(len(l.elts) for l in layers) * int(yet.offsets[-1])
+    for lay, y in zip(layers, fused):
+        single = run_aggregate_analysis([lay], yet)[0].losses
+        assert y.losses.tobytes() == single.tobytes()
+        assert y.layer_id == lay.id
+    small = yet.head(300)
+    for lay in layers[:3]:
+        want = _oracle_ylt(lay, small)
+        got = run_aggregate_analysis(layers[:3], small)[layers.index(lay)].losses
+        assert got.tobytes() == want.tobytes()

@@ -215,3 +215,17 @@ def test_library_loads_and_reports_without_gpu():
     if rc != 0:  # no GPU here: the call fails loudly instead of pretending
         assert _native.last_error()
     assert _native.launch_count() >= 0
+
+
+# ------------------------------------------------------- multi-layer pool --
+
+def test_layer_pool_orders_and_masks():
+    from paper_1308_2066_b200.engine import layer_pool
+
+    a, b, c, d = (EventLossTable.from_records({i + 1: 1.0}, 10) for i in range(4))
+    pool, masks = layer_pool([Layer("x", (a, c)), Layer("y", (b, c, d)), Layer("z", (a, b))])
+    assert [pool.index(e) for e in (a, b, c, d)] == [0, 1, 2, 3]
+    assert masks == [0b0101, 0b1110, 0b0011]
+    # a layer that orders c before a conflicts with a layer ordering a before c
+    assert layer_pool([Layer("x", (a, c)), Layer("y", (c, a))]) is None
+    assert layer_pool([Layer("x", (a, a))]) is None
