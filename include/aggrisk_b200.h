@@ -109,6 +109,14 @@ int are_plan_build_pool(are_tables_t t, const int64_t *rows, int64_t n_sel,
                         const double *fin_rate, const double *fin_ret,
                         const double *fin_lim, const double *fin_share,
                         are_plan_t *out);
+/* Pre-combined plan: K1 folds each event's losses through
+ * the financial terms once (comb = 0.0 + sum_j fin_j(x_j), selection order),
+ * so K2 reads one value per hot event.  A different unit of work from the
+ * per-lookup path -- reported separately, never as the headline. */
+int are_plan_build_precombined(are_tables_t t, const int64_t *rows, int64_t n_sel,
+                               const double *fin_rate, const double *fin_ret,
+                               const double *fin_lim, const double *fin_share,
+                               are_plan_t *out);
 int are_plan_info(are_plan_t p, are_plan_info_t *info);
 int are_plan_free(are_plan_t p);
 

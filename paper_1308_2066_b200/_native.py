@@ -73,6 +73,7 @@ SIGNATURES = {
     "are_tables_free": (ctypes.c_int, [_P]),
     "are_plan_build": (ctypes.c_int, [_P, _P, _I64, _P, _P, _P, _P, ctypes.POINTER(_P)]),
     "are_plan_build_pool": (ctypes.c_int, [_P, _P, _I64, _P, _P, _P, _P, ctypes.POINTER(_P)]),
+    "are_plan_build_precombined": (ctypes.c_int, [_P, _P, _I64, _P, _P, _P, _P, ctypes.POINTER(_P)]),
     "are_plan_info": (ctypes.c_int, [_P, ctypes.POINTER(PlanInfo)]),
     "are_plan_free": (ctypes.c_int, [_P]),
     "are_simulate_device": (
@@ -199,13 +200,14 @@ def read_row(tables: Handle, row: int, row_len: int) -> np.ndarray:
     return out
 
 
-def plan_build(tables: Handle, rows, rate, ret, lim, share, pool: bool = False) -> Handle:
+def plan_build(tables: Handle, rows, rate, ret, lim, share, pool: bool = False,
+               precombine: bool = False) -> Handle:
     lib = load()
     arrs = [np.ascontiguousarray(rows, dtype=np.int64)] + [
         np.ascontiguousarray(x, dtype=np.float64) for x in (rate, ret, lim, share)
     ]
     out = _P()
-    fn = lib.are_plan_build_pool if pool else lib.are_plan_build
+    fn = lib.are_plan_build_pool if pool else (lib.are_plan_build_precombined if precombine else lib.are_plan_build)
     check(fn(tables.value, ptr(arrs[0]), arrs[0].shape[0], *(ptr(x) for x in arrs[1:]), ctypes.byref(out)))
     return Handle(out.value, "are_plan_free")
 

@@ -88,6 +88,7 @@ struct are_plan_s {
     bool zero_skip = false;
     bool slot0_hot = false;
     bool pool = false;
+    bool precombined = false;
     unsigned int *d_err = nullptr;
     size_t smem = 0;
 };
@@ -225,6 +226,7 @@ static void fill_args(const are_plan_s *p, K2Args &a, double occ_ret, double occ
     a.agg_lim = agg_lim;
     a.stacked = p->tab->d;
     a.rows = p->d_rows;
+    a.precombined = p->precombined ? 1 : 0;
 }
 
 }  // namespace are
@@ -393,7 +395,7 @@ int are_tables_free(are_tables_t t) {
 // ---- plan -------------------------------------------------------------------
 static int plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
                       const double *fin_ret, const double *fin_lim, const double *fin_share, bool pool,
-                      are_plan_t *out) {
+                      bool precombine, are_plan_t *out) {
     if (!t) return fail(ARE_EINVAL, "null tables handle");
     if (n_sel < 1) return fail(ARE_EINVAL, "table selection is empty");
     if (n_sel > ARE_MAX_TABLES)
@@ -440,6 +442,10 @@ static int plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const 
     cudaMemcpyAsync(p->d_fin, hf.data(), n_sel * sizeof(Fin), cudaMemcpyHostToDevice, st);
     cudaMemsetAsync(p->d_err, 0, sizeof(unsigned int), st);
     rc = k1_build_plan(t->d, t->row_len, p->d_rows, (int)n_sel, p->nbits, p->pb, di->sms, st);
+    if (rc == ARE_OK && precombine) {
+        rc = k1_precombine_plan(p->pb, p->d_fin, t->row_len, di->sms, st);
+        p->precombined = true;
+    }
     Slot slot0{};
     if (rc == ARE_OK) {
         cudaError_t ce = cudaMemcpyAsync(&slot0, p->pb.slots, sizeof(Slot), cudaMemcpyDeviceToHost, st);
@@ -462,12 +468,18 @@ static int plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const 
 
 int are_plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
                    const double *fin_ret, const double *fin_lim, const double *fin_share, are_plan_t *out) {
-    return plan_build(t, rows, n_sel, fin_rate, fin_ret, fin_lim, fin_share, false, out);
+    return plan_build(t, rows, n_sel, fin_rate, fin_ret, fin_lim, fin_share, false, false, out);
+}
+
+int are_plan_build_precombined(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
+                               const double *fin_ret, const double *fin_lim, const double *fin_share,
+                               are_plan_t *out) {
+    return plan_build(t, rows, n_sel, fin_rate, fin_ret, fin_lim, fin_share, false, true, out);
 }
 
 int are_plan_build_pool(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
                         const double *fin_ret, const double *fin_lim, const double *fin_share, are_plan_t *out) {
-    return plan_build(t, rows, n_sel, fin_rate, fin_ret, fin_lim, fin_share, true, out);
+    return plan_build(t, rows, n_sel, fin_rate, fin_ret, fin_lim, fin_share, true, false, out);
 }
 
 int are_plan_info(are_plan_t p, are_plan_info_t *info) {

@@ -20,6 +20,8 @@
 
 namespace are {
 
+static unsigned grid_for(int64_t n, int threads, int sms, int per_sm = 8);
+
 // ---- (1) dense tables ----------------------------------------------------
 
 // blockIdx.y = table; scatter table y's records into its dense row.
@@ -126,6 +128,34 @@ __global__ void k1_filter(const Slot *__restrict__ slots, int64_t row_len, int64
     }
 }
 
+// Pre-combination: fold every hot event's entries
+// into its combined loss comb = 0.0 + sum_j fin_j(x_j) (selection order, the
+// same _rn operations K2 performs), stored in the record's x with count 1.
+// K2 then skips the financial terms; results stay bit-identical.
+__global__ void k1_precombine(Slot *__restrict__ slots, const Entry *__restrict__ ovf, const Fin *__restrict__ fin,
+                              int64_t row_len) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < row_len;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        Slot s = slots[e];
+        const uint32_t cnt = s.meta >> 16;
+        if (!cnt) continue;
+        double comb = __dadd_rn(0.0, fin_term(fin[s.meta & 0xFFFFu], s.x));
+        for (uint32_t i = 1; i < cnt; ++i) {
+            const Entry en = ovf[s.ovf + i - 1];
+            comb = __dadd_rn(comb, fin_term(fin[en.j], en.x));
+        }
+        s.x = comb;
+        s.meta = 1u << 16;
+        slots[e] = s;
+    }
+}
+
+int k1_precombine_plan(PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int sms, cudaStream_t st) {
+    k1_precombine<<<grid_for(row_len, 256, sms), 256, 0, st>>>(pb.slots, pb.ovf, d_fin, row_len);
+    ARE_LAUNCHED();
+    return ARE_OK;
+}
+
 // ---- exclusive scan of uint32 counts (3 passes, deterministic) ------------
 static constexpr int SCAN_THREADS = 1024;
 static constexpr int SCAN_ITEMS = 4;
@@ -215,7 +245,7 @@ int scan_exclusive_u32(const uint32_t *d_in, uint32_t *d_out, int64_t n, uint64_
 
 // ---- host drivers --------------------------------------------------------
 
-static unsigned grid_for(int64_t n, int threads, int sms, int per_sm = 8) {
+static unsigned grid_for(int64_t n, int threads, int sms, int per_sm) {
     int64_t g = (n + threads - 1) / threads;
     int64_t cap = (int64_t)sms * per_sm;
     if (g > cap) g = cap;

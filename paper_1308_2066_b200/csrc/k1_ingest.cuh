@@ -20,6 +20,8 @@ int k1_scatter(const uint32_t *d_ids, const double *d_losses, const int64_t *d_t
 int k1_build_plan(const double *d_stacked, int64_t row_len, const int64_t *d_rows, int n_sel,
                   int64_t filter_bits, PlanBuffers &pb, int sms, cudaStream_t st);
 
+int k1_precombine_plan(PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int sms, cudaStream_t st);
+
 int scan_exclusive_u32(const uint32_t *d_in, uint32_t *d_out, int64_t n, uint64_t *d_tiles,
                        uint64_t *h_total, cudaStream_t st);
 

@@ -52,7 +52,7 @@ __device__ __forceinline__ uint32_t hot_hash(uint32_t e, uint32_t nbits) {
 // folds the 32 occurrence values into c strictly in order.
 // CHECK = false when the caller has validated every id <= catalog (the
 // reference's validate_portfolio, or DeviceYearEventTable's upload check).
-template <int HASH, bool CHECK>
+template <int HASH, bool CHECK, bool PRE>
 __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
     constexpr int NW = K2_THREADS / 32;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -92,11 +92,15 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
         if ((uint32_t)lane < n) {
             const uint32_t cnt = s.meta >> 16;
             double comb = 0.0;
-            if (cnt) comb = __dadd_rn(0.0, fin_term(s_fin[s.meta & 0xFFFFu], s.x));
+            if (PRE) {  // pre-combined plan: x already holds comb
+                if (cnt) comb = s.x;
+            } else {
+                if (cnt) comb = __dadd_rn(0.0, fin_term(s_fin[s.meta & 0xFFFFu], s.x));
 #pragma unroll 1
-            for (uint32_t i = 1; i < cnt; ++i) {  // events in several tables (~7%)
-                const Entry en = a.ovf[s.ovf + i - 1];
-                comb = __dadd_rn(comb, fin_term(s_fin[en.j], en.x));
+                for (uint32_t i = 1; i < cnt; ++i) {  // events in several tables (~7%)
+                    const Entry en = a.ovf[s.ovf + i - 1];
+                    comb = __dadd_rn(comb, fin_term(s_fin[en.j], en.x));
+                }
             }
             ob[lane] = clamp_ref(__dsub_rn(comb, occ_ret), occ_lim);
         }
@@ -260,20 +264,40 @@ size_t k2_hotset_fixed_smem(int n_sel) {
     return (size_t)n_sel * sizeof(Fin) + (size_t)NW * 32 * sizeof(double) + (size_t)NW * QCAP * sizeof(uint32_t);
 }
 
-template <int HASH, bool CHECK>
+template <int HASH, bool CHECK, bool PRE>
 static int prepare_one() {
-    ARE_CUDA(cudaFuncSetAttribute(k2_hotset<HASH, CHECK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ARE_CUDA(cudaFuncSetAttribute(k2_hotset<HASH, CHECK, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   k2_max_dynamic_smem()));
+    return ARE_OK;
+}
+
+template <bool PRE>
+static int prepare_pre() {
+    int rc;
+    if ((rc = prepare_one<0, true, PRE>()) || (rc = prepare_one<1, true, PRE>()) ||
+        (rc = prepare_one<2, true, PRE>()) || (rc = prepare_one<0, false, PRE>()) ||
+        (rc = prepare_one<1, false, PRE>()) || (rc = prepare_one<2, false, PRE>()))
+        return rc;
     return ARE_OK;
 }
 
 int k2_prepare(int device) {
     (void)device;
     int rc;
-    if ((rc = prepare_one<0, true>()) || (rc = prepare_one<1, true>()) || (rc = prepare_one<2, true>()) ||
-        (rc = prepare_one<0, false>()) || (rc = prepare_one<1, false>()) || (rc = prepare_one<2, false>()))
-        return rc;
+    if ((rc = prepare_pre<false>()) || (rc = prepare_pre<true>())) return rc;
     return k2_layers_prepare();
+}
+
+template <bool PRE>
+static void launch_hotset(const K2Args &a, int sel, dim3 grid, dim3 block, size_t smem, cudaStream_t st) {
+    switch (sel) {
+        case 0: k2_hotset<0, false, PRE><<<grid, block, smem, st>>>(a); break;
+        case 1: k2_hotset<0, true, PRE><<<grid, block, smem, st>>>(a); break;
+        case 2: k2_hotset<1, false, PRE><<<grid, block, smem, st>>>(a); break;
+        case 3: k2_hotset<1, true, PRE><<<grid, block, smem, st>>>(a); break;
+        case 4: k2_hotset<2, false, PRE><<<grid, block, smem, st>>>(a); break;
+        default: k2_hotset<2, true, PRE><<<grid, block, smem, st>>>(a); break;
+    }
 }
 
 int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStream_t st) {
@@ -293,14 +317,10 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
     if (g > sms) g = sms;  // persistent: one CTA per SM (the filter fills shared memory)
     const dim3 grid((unsigned)g), block(K2_THREADS);
     const int sel = a.hash_mode * 2 + (check ? 1 : 0);
-    switch (sel) {
-        case 0: k2_hotset<0, false><<<grid, block, smem_bytes, st>>>(a); break;
-        case 1: k2_hotset<0, true><<<grid, block, smem_bytes, st>>>(a); break;
-        case 2: k2_hotset<1, false><<<grid, block, smem_bytes, st>>>(a); break;
-        case 3: k2_hotset<1, true><<<grid, block, smem_bytes, st>>>(a); break;
-        case 4: k2_hotset<2, false><<<grid, block, smem_bytes, st>>>(a); break;
-        default: k2_hotset<2, true><<<grid, block, smem_bytes, st>>>(a); break;
-    }
+    if (a.precombined)
+        launch_hotset<true>(a, sel, grid, block, smem_bytes, st);
+    else
+        launch_hotset<false>(a, sel, grid, block, smem_bytes, st);
     ARE_LAUNCHED();
     return ARE_OK;
 }

@@ -32,6 +32,7 @@ struct K2Args {
     const double *stacked;
     const int64_t *rows;
     unsigned int *err;
+    int32_t precombined;   // records hold comb (k1_precombine): skip the financial terms
 };
 
 // Threads per CTA of the hot-set kernel (one persistent CTA per SM).

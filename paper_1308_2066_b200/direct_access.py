@@ -176,10 +176,11 @@ class TableSet:
         return (sel, np.ascontiguousarray(self.fin_rate[sel]), np.ascontiguousarray(self.fin_ret[sel]),
                 np.ascontiguousarray(self.fin_lim[sel]), np.ascontiguousarray(self.fin_share[sel]))
 
-    def plan(self, rows, rate, ret, lim, share, pool: bool = False) -> _native.Handle:
+    def plan(self, rows, rate, ret, lim, share, pool: bool = False, precombine: bool = False) -> _native.Handle:
         """Device hot set for this selection + financial terms (cached, LRU);
-        `pool` sizes it for the fused multi-layer kernel."""
-        key = (pool, np.asarray(rows, np.int64).tobytes(),
+        `pool` sizes it for the fused multi-layer kernel; `precombine` folds
+        the financial terms into one value per event."""
+        key = (pool, precombine, np.asarray(rows, np.int64).tobytes(),
                np.asarray(rate, np.float64).tobytes(), np.asarray(ret, np.float64).tobytes(),
                np.asarray(lim, np.float64).tobytes(), np.asarray(share, np.float64).tobytes())
         with self._lock:
@@ -187,7 +188,7 @@ class TableSet:
             if hit is not None:
                 self._plans.move_to_end(key)
                 return hit
-        plan = _native.plan_build(self._dev, rows, rate, ret, lim, share, pool=pool)
+        plan = _native.plan_build(self._dev, rows, rate, ret, lim, share, pool=pool, precombine=precombine)
         with self._lock:
             self._plans[key] = plan
             while len(self._plans) > _PLAN_CACHE:

@@ -56,6 +56,7 @@ class EngineConfig:
     deterministic: bool = True
     backend: str = "auto"
     variant: str = "auto"
+    precombine: bool = False  # one combined value per hot event (K1 folds the terms)
 
     def __post_init__(self):
         if self.worker_count < 1:
@@ -230,7 +231,7 @@ def _simulate(yet, tset: TableSet, selection, terms: LayerTerms, cfg: EngineConf
     n = int(yet.offsets.shape[0]) - 1
     if n == 0:
         return 0
-    plan = tset.plan(rows, rate, ret, lim, share)
+    plan = tset.plan(rows, rate, ret, lim, share, precombine=cfg.precombine)
     resident = getattr(yet, "_device", None)
     if resident is not None:  # DeviceYearEventTable: ids already in HBM
         return resident.simulate(plan, rows.shape[0], terms, out, cfg.variant)
@@ -318,7 +319,7 @@ def simulate_layers_device(dyet, pool_tset: TableSet, masks, terms_list, out=Non
 
 
 def _fusable(layers: Sequence[Layer], cfg: EngineConfig):
-    if len(layers) < 2 or cfg.variant not in ("auto", "hotset"):
+    if len(layers) < 2 or cfg.variant not in ("auto", "hotset") or cfg.precombine:
         return None
     got = layer_pool(layers)
     if got is None:
