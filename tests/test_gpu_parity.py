@@ -410,3 +410,44 @@ def test_fused_layers_bitwise_equal_single_layer_runs():
         want = _oracle_ylt(lay, small)
         got = run_aggregate_analysis(layers[:3], small)[layers.index(lay)].losses
         assert got.tobytes() == want.tobytes()
+
+
+# ------------------------------------------------- the C ABI drop-in itself --
+
+def test_c_abi_are_run_trials_matches_reference(instances):
+    """are_run_trials: the reference run_trials argument list flattened to
+    pointers (include/aggrisk_b200.h), as a cgo/ctypes binding would call it."""
+    import ctypes
+
+    lib = _native.load()
+    for inst in instances[:200]:
+        stacked = np.ascontiguousarray(inst.stacked)
+        rows = np.arange(len(inst.layer.elts), dtype=np.int64)
+        fin = [np.ascontiguousarray(a, dtype=np.float64) for a in inst.fin()]
+        out = np.full(inst.yet.trial_count, -1.0)
+        t = inst.layer.terms
+        lookups = ctypes.c_int64()
+        rc = lib.are_run_trials(inst.yet.event_ids.ctypes.data, inst.yet.event_ids.size,
+                                inst.yet.offsets.ctypes.data, inst.yet.offsets.size,
+                                stacked.ctypes.data, stacked.shape[0], stacked.shape[1],
+                                rows.ctypes.data, rows.size, *(a.ctypes.data for a in fin),
+                                t.occ_retention, t.occ_limit, t.agg_retention, t.agg_limit,
+                                0, 0, inst.yet.trial_count, out.ctypes.data, 1, ctypes.byref(lookups))
+        assert rc == 0, _native.last_error()
+        assert out.tobytes() == inst.ylt.tobytes()
+        assert lookups.value == rows.size * int(inst.yet.offsets[-1])
+    # reference argument errors (_kernel.pyx:49-52) map to ARE_EINVAL
+    inst = instances[0]
+    stacked = np.ascontiguousarray(inst.stacked)
+    rows = np.zeros(300, dtype=np.int64)
+    ones = np.ones(300)
+    rc = lib.are_run_trials(inst.yet.event_ids.ctypes.data, inst.yet.event_ids.size, inst.yet.offsets.ctypes.data,
+                            inst.yet.offsets.size, stacked.ctypes.data, stacked.shape[0], stacked.shape[1],
+                            rows.ctypes.data, 300, *(ones.ctypes.data for _ in range(4)), 0.0, 1.0, 0.0, 1.0,
+                            0, 0, 1, np.empty(inst.yet.trial_count).ctypes.data, 1, None)
+    assert rc == _native.ARE_EINVAL and "256" in _native.last_error()
+    rc = lib.are_run_trials(inst.yet.event_ids.ctypes.data, inst.yet.event_ids.size, inst.yet.offsets.ctypes.data,
+                            inst.yet.offsets.size, stacked.ctypes.data, stacked.shape[0], stacked.shape[1],
+                            rows.ctypes.data, 1, *(ones.ctypes.data for _ in range(4)), 0.0, 1.0, 0.0, 1.0,
+                            8, 0, 1, np.empty(inst.yet.trial_count).ctypes.data, 4, None)
+    assert rc == _native.ARE_EINVAL and "scratch" in _native.last_error()
