@@ -8,17 +8,24 @@
 //
 // Device algorithm: one cooperative launch.  MSD radix select on the
 // order-preserving 64-bit key of each float64 (NaN last, like np.partition),
-// 8 passes of 8 bits, all return periods of a call selected together (one
-// 256-bin histogram per rp and pass: shared-memory atomics, one global add
-// per bin, a grid barrier, then every CTA fixes the next digit itself).  The tail sum is
-// then  S = sum of losses strictly above the PML key  (double-double
-// accumulation, fixed grid, partials combined in a fixed order, so the
-// result is bit-reproducible run to run and for any GPU count) plus
-// (m - G) copies of the PML value itself (G = count strictly above):
+// six passes of 11/11/11/11/11/9 bits, up to 8 return periods selected
+// together.  Pass 0 builds ONE histogram all return periods share (no prefix
+// yet); later passes build one per distinct prefix (return periods whose
+// prefixes agree -- ties, e.g. several PMLs at an aggregate limit -- share
+// it).  Shared-memory atomics, one global add per non-empty bin, a grid
+// barrier, then every CTA fixes the next digit itself.  One tail pass then
+// accumulates, for every return period at once,
+//     S = sum of losses strictly above the PML key
+// in double-double (warp trees, a block tree, and a last-block combine of
+// the per-CTA partials -- a fixed order for a fixed grid, so the result is
+// bit-reproducible run to run) plus (m - G) copies of the PML value itself
+// (G = count strictly above):
 //     tvar = (S + (m - G) * pml) / m.
 // This equals the mean of the closed tail for any ties; it is within a few
 // ulp of numpy's pairwise mean (tolerance in tests/test_metrics_gpu.py).
 #include "k3_order_stats.cuh"
+
+#include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cmath>
@@ -29,8 +36,14 @@
 
 namespace are {
 
-static constexpr int K3_MAX_RP = 16;
+static constexpr int K3_GROUP = 8;       // return periods per launch
 static constexpr int K3_THREADS = 512;
+static constexpr int K3_BINS = 2048;     // 11-bit digits
+static constexpr int K3_PASSES = 6;      // 11, 11, 11, 11, 11, 9 bits
+static constexpr int K3_TAIL = 4;        // return periods per tail sweep
+
+__host__ __device__ constexpr int k3_shift(int pass) { return pass < 5 ? 53 - 11 * pass : 0; }
+__host__ __device__ constexpr int k3_width(int pass) { return pass < 5 ? 11 : 9; }
 
 struct DD {
     double hi, lo;
@@ -42,6 +55,22 @@ __device__ __forceinline__ void dd_add(DD &a, double b) {
     a.hi = s;
     a.lo = __dadd_rn(a.lo, err);
 }
+__device__ __forceinline__ void dd_merge(DD &a, const DD &b) {
+    dd_add(a, b.hi);
+    a.lo = __dadd_rn(a.lo, b.lo);
+}
+// Fixed-shape warp tree: lane 0 ends with the combined value.
+__device__ __forceinline__ void dd_warp_reduce(DD &a, unsigned long long &cnt) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        DD b;
+        b.hi = __shfl_down_sync(0xffffffffu, a.hi, o);
+        b.lo = __shfl_down_sync(0xffffffffu, a.lo, o);
+        const unsigned long long c = __shfl_down_sync(0xffffffffu, cnt, o);
+        dd_merge(a, b);
+        cnt += c;
+    }
+}
 
 struct TailPartial {
     double hi, lo;
@@ -49,149 +78,253 @@ struct TailPartial {
     unsigned long long pad;
 };
 
-// Device workspace of one K3 call; zeroed (hist, barrier) before launch.
-struct K3Work {
-    unsigned int hist[3][K3_MAX_RP][256];  // triple-buffered pass histograms
-    unsigned int bar_count, bar_gen;
-    int64_t rank[K3_MAX_RP];               // 1-based ranks k (input)
-    int64_t m_tail[K3_MAX_RP];             // n - k + 1 (input)
-    double res[2][K3_MAX_RP];              // pml, tvar (output)
+struct K3Params {
+    int64_t rank[K3_GROUP];    // 1-based ranks k
+    int64_t m_tail[K3_GROUP];  // n - k + 1
+    int n_rp;
 };
 
-// Sense-free generation barrier across a co-resident (cooperative) grid.
-__device__ __forceinline__ void grid_barrier(unsigned int *count, unsigned int *gen) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned int *vgen = gen;
-        const unsigned int g = *vgen;
-        __threadfence();
-        if (atomicAdd(count, 1u) == gridDim.x - 1) {
-            *count = 0;
-            __threadfence();
-            atomicAdd(gen, 1u);
-        } else {
-            while (*vgen == g) __nanosleep(32);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
+// Device workspace of one K3 call; cleared (cudaMemsetAsync) before launch.
+struct K3Work {
+    unsigned int hist[3][K3_GROUP][K3_BINS];  // triple-buffered pass histograms
+    unsigned int bar_count, bar_gen, done, pad;
+    double res[2][K3_GROUP];                  // pml, tvar (output)
+};
 
-// One cooperative launch: 8 MSD radix passes (8-bit digits) selecting the
-// k-th smallest key for every return period, then the tail sums.
-__global__ void __launch_bounds__(K3_THREADS) k3_select(const double *__restrict__ x, int64_t n, int n_rp,
-                                                       K3Work *__restrict__ w, TailPartial *__restrict__ part) {
-    __shared__ unsigned int sh[K3_MAX_RP * 256];
-    __shared__ uint64_t s_prefix[K3_MAX_RP];
-    __shared__ uint64_t s_rank[K3_MAX_RP];
+__global__ void __launch_bounds__(K3_THREADS, 2) k3_select(const double *__restrict__ x, int64_t n, const K3Params prm,
+                                                          K3Work *__restrict__ w, TailPartial *__restrict__ part) {
+    extern __shared__ unsigned int sh[];  // [K3_GROUP][K3_BINS]
+    __shared__ uint64_t s_prefix[K3_GROUP];
+    __shared__ uint64_t s_rank[K3_GROUP];
+    __shared__ uint64_t s_lpre[K3_GROUP];  // distinct prefixes ("leaders")
+    __shared__ int s_slot[K3_GROUP];       // rp -> its leader's histogram row
+    __shared__ int s_nlead;
+    __shared__ DD s_dd[K3_THREADS / 32][K3_TAIL];
+    __shared__ unsigned long long s_cnt[K3_THREADS / 32][K3_TAIL];
+    __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid < n_rp) {
+    const int R = prm.n_rp;
+    if (tid < R) {
         s_prefix[tid] = 0;
-        s_rank[tid] = (uint64_t)w->rank[tid];
+        s_rank[tid] = (uint64_t)prm.rank[tid];
+        s_slot[tid] = 0;
+        s_lpre[tid] = 0;
     }
+    if (tid == 0) s_nlead = 1;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int pass = 0; pass < 8; ++pass) {
-        const int shift = 56 - 8 * pass;
-        const uint64_t hi_mask = pass == 0 ? 0ull : (~0ull << (shift + 8));
-        for (int i = tid; i < n_rp * 256; i += blockDim.x) sh[i] = 0;
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + tid;
+    for (int pass = 0; pass < K3_PASSES; ++pass) {
+        const int shift = k3_shift(pass), nb = 1 << k3_width(pass);
+        const uint64_t hi_mask = pass == 0 ? 0ull : (~0ull << (shift + k3_width(pass)));
         __syncthreads();
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + tid; i < n; i += stride) {
-            const uint64_t k = order_key(x[i]);
-            const unsigned d = (unsigned)(k >> shift) & 255u;
-            for (int r = 0; r < n_rp; ++r)
-                if (((k ^ s_prefix[r]) & hi_mask) == 0) atomicAdd(&sh[r * 256 + d], 1u);
+        const int rows = s_nlead;
+        for (int i = tid; i < rows * nb; i += blockDim.x) sh[i] = 0;
+        __syncthreads();
+        if (pass == 0) {
+            int64_t i = i0;
+            for (; i + 3 * stride < n; i += 4 * stride) {
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = __ldg(x + i + u * stride);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) atomicAdd(&sh[(unsigned)(order_key(v[u]) >> shift)], 1u);
+            }
+            for (; i < n; i += stride) atomicAdd(&sh[(unsigned)(order_key(__ldg(x + i)) >> shift)], 1u);
+        } else {
+            uint64_t pre[K3_GROUP];
+#pragma unroll
+            for (int j = 0; j < K3_GROUP; ++j) pre[j] = j < rows ? s_lpre[j] : 0;
+            auto count = [&](double v) {
+                const uint64_t k = order_key(v);
+                const unsigned d = (unsigned)(k >> shift) & (unsigned)(nb - 1);
+#pragma unroll
+                for (int j = 0; j < K3_GROUP; ++j) {
+                    if (j >= rows) break;
+                    if (((k ^ pre[j]) & hi_mask) == 0) atomicAdd(&sh[j * nb + d], 1u);
+                }
+            };
+            int64_t i = i0;
+            for (; i + 3 * stride < n; i += 4 * stride) {
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = __ldg(x + i + u * stride);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) count(v[u]);
+            }
+            for (; i < n; i += stride) count(__ldg(x + i));
         }
         __syncthreads();
-        unsigned int(*h)[256] = w->hist[pass % 3];
-        for (int i = tid; i < n_rp * 256; i += blockDim.x)
-            if (sh[i]) atomicAdd(&h[i >> 8][i & 255], sh[i]);
-        grid_barrier(&w->bar_count, &w->bar_gen);
+        unsigned int(*h)[K3_BINS] = w->hist[pass % 3];
+        for (int i = tid; i < rows * nb; i += blockDim.x)
+            if (sh[i]) atomicAdd(&h[i / nb][i % nb], sh[i]);
+        cooperative_groups::this_grid().sync();
         if (blockIdx.x == 0)  // buffer of pass+2 was last read before this barrier
-            for (int i = tid; i < n_rp * 256; i += blockDim.x) w->hist[(pass + 2) % 3][i >> 8][i & 255] = 0;
-        // every CTA fixes the next digit itself: warp r scans rp r's 256 bins
-        if (warp < n_rp) {
-            const volatile unsigned int *hr = h[warp];
-            uint64_t cnt[8], tot = 0;
+            for (int i = tid; i < R * K3_BINS; i += blockDim.x) w->hist[(pass + 2) % 3][i / K3_BINS][i % K3_BINS] = 0;
+        // stage the global histogram rows in shared memory (one round trip)
+        {
+            const int q = nb >> 2;  // uint4 per row
+            for (int i = tid; i < rows * q; i += blockDim.x)
+                reinterpret_cast<uint4 *>(sh)[i] = __ldcg(reinterpret_cast<const uint4 *>(h[i / q]) + (i % q));
+        }
+        __syncthreads();
+        // every CTA fixes the next digit itself: warp r scans rp r's row
+        if (warp < R) {
+            const unsigned int *hr = sh + s_slot[warp] * nb;
+            const int per = nb >> 5;  // bins per lane: 64 or 16
+            const uint4 *mine = reinterpret_cast<const uint4 *>(hr + lane * per);
+            uint64_t tot = 0;
 #pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                cnt[b] = hr[lane * 8 + b];
-                tot += cnt[b];
-            }
+            for (int b = 0; b < 16; ++b)
+                if (4 * b < per) {
+                    const uint4 v = mine[b];
+                    tot += (uint64_t)v.x + v.y + v.z + v.w;
+                }
             uint64_t inc = tot;
+#pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint64_t v = __shfl_up_sync(0xffffffffu, inc, o);
                 if (lane >= o) inc += v;
             }
             const uint64_t want = s_rank[warp];
-            uint64_t run = inc - tot;  // bins before this lane's 8
-            const bool mine = run < want && want <= inc;
-            const unsigned owner = __ballot_sync(0xffffffffu, mine);
-            if (mine) {
-                int b = 0;
-                for (; b < 7 && run + cnt[b] < want; ++b) run += cnt[b];
-                s_rank[warp] = want - run;
-                s_prefix[warp] |= (uint64_t)(lane * 8 + b) << shift;
+            // the lane whose bins cross `want`, then the warp searches its
+            // bins 32 at a time (shuffle scan, ballot)
+            const unsigned owner_mask = __ballot_sync(0xffffffffu, inc - tot < want && want <= inc);
+            const int owner = __ffs(owner_mask) - 1;
+            uint64_t run = __shfl_sync(0xffffffffu, inc - tot, owner);
+            const unsigned int *ob = hr + owner * per;
+            for (int b0 = 0; b0 < per; b0 += 32) {
+                const uint64_t c = lane < per - b0 ? ob[b0 + lane] : 0u;
+                uint64_t ci = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t v = __shfl_up_sync(0xffffffffu, ci, o);
+                    if (lane >= o) ci += v;
+                }
+                const unsigned hit = __ballot_sync(0xffffffffu, run + ci >= want);
+                if (hit) {
+                    const int l = __ffs(hit) - 1;
+                    const uint64_t before = run + __shfl_sync(0xffffffffu, ci - c, l);
+                    if (lane == 0) {
+                        s_rank[warp] = want - before;
+                        s_prefix[warp] |= (uint64_t)(owner * per + b0 + l) << shift;
+                    }
+                    break;
+                }
+                run += __shfl_sync(0xffffffffu, ci, 31);
             }
-            (void)owner;
+        }
+        __syncthreads();
+        if (tid == 0) {  // equal prefixes share one histogram row next pass
+            int nl = 0;
+            for (int r = 0; r < R; ++r) {
+                int j = 0;
+                while (j < nl && s_lpre[j] != s_prefix[r]) ++j;
+                if (j == nl) s_lpre[nl++] = s_prefix[r];
+                s_slot[r] = j;
+            }
+            s_nlead = nl;
+        }
+    }
+    // tail: sum and count of losses strictly above each PML key, K3_TAIL
+    // return periods per sweep
+    for (int r0 = 0; r0 < R; r0 += K3_TAIL) {
+        uint64_t kp[K3_TAIL];
+        DD acc[K3_TAIL];
+        unsigned long long above[K3_TAIL];
+#pragma unroll
+        for (int r = 0; r < K3_TAIL; ++r) {
+            kp[r] = r0 + r < R ? s_prefix[r0 + r] : ~0ull;  // ~0: nothing is above
+            acc[r] = DD{0.0, 0.0};
+            above[r] = 0;
+        }
+        auto tail = [&](double v) {
+            const uint64_t k = order_key(v);
+#pragma unroll
+            for (int r = 0; r < K3_TAIL; ++r)
+                if (k > kp[r]) {
+                    dd_add(acc[r], v);
+                    ++above[r];
+                }
+        };
+        int64_t i = i0;
+        for (; i + 3 * stride < n; i += 4 * stride) {
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldg(x + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) tail(v[u]);
+        }
+        for (; i < n; i += stride) tail(__ldg(x + i));
+#pragma unroll
+        for (int r = 0; r < K3_TAIL; ++r) {
+            dd_warp_reduce(acc[r], above[r]);
+            if (lane == 0) {
+                s_dd[warp][r] = acc[r];
+                s_cnt[warp][r] = above[r];
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+#pragma unroll
+            for (int r = 0; r < K3_TAIL; ++r) {
+                DD a = {0.0, 0.0};
+                unsigned long long c = 0;
+                if (lane < K3_THREADS / 32) {
+                    a = s_dd[lane][r];
+                    c = s_cnt[lane][r];
+                }
+                dd_warp_reduce(a, c);
+                if (lane == 0 && r0 + r < R)
+                    part[(int64_t)(r0 + r) * gridDim.x + blockIdx.x] = TailPartial{a.hi, a.lo, c, 0};
+            }
         }
         __syncthreads();
     }
-    // tail: sum and count of losses strictly above each PML key
-    for (int r = 0; r < n_rp; ++r) {
-        const uint64_t kp = s_prefix[r];
-        DD acc = {0.0, 0.0};
-        unsigned long long above = 0;
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + tid; i < n; i += stride) {
-            const double v = x[i];
-            if (order_key(v) > kp) {
-                dd_add(acc, v);
-                ++above;
-            }
-        }
-        __shared__ double shi[K3_THREADS], slo[K3_THREADS];
-        __shared__ unsigned long long sab[K3_THREADS];
-        shi[tid] = acc.hi;
-        slo[tid] = acc.lo;
-        sab[tid] = above;
-        __syncthreads();
-        if (tid == 0) {  // fixed-order block combine
-            DD b = {0.0, 0.0};
-            unsigned long long ab = 0;
-            for (int i = 0; i < (int)blockDim.x; ++i) {
-                dd_add(b, shi[i]);
-                b.lo = __dadd_rn(b.lo, slo[i]);
-                ab += sab[i];
-            }
-            part[(int64_t)r * gridDim.x + blockIdx.x] = TailPartial{b.hi, b.lo, ab, 0};
-        }
-        __syncthreads();
-    }
-    grid_barrier(&w->bar_count, &w->bar_gen);
-    if (blockIdx.x == 0 && tid < n_rp) {  // fixed-order grid combine
-        const int r = tid;
+    // the last CTA to finish combines the partials
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&w->done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp < R) {
+        const int r = warp;
         DD s = {0.0, 0.0};
-        unsigned long long above = 0;
-        for (int b = 0; b < (int)gridDim.x; ++b) {
-            const TailPartial p = part[(int64_t)r * gridDim.x + b];
-            dd_add(s, p.hi);
-            s.lo = __dadd_rn(s.lo, p.lo);
-            above += p.above;
+        unsigned long long ab = 0;
+        for (int b0 = 0; b0 < (int)gridDim.x; b0 += 32 * 8) {  // loads first, then merge
+            double2 v[8];
+            unsigned long long c[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int b = b0 + 32 * u + lane;
+                const TailPartial *pp = part + (int64_t)r * gridDim.x + b;
+                v[u] = b < (int)gridDim.x ? __ldcg(reinterpret_cast<const double2 *>(pp)) : make_double2(0.0, 0.0);
+                c[u] = b < (int)gridDim.x ? __ldcg(&pp->above) : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                dd_merge(s, DD{v[u].x, v[u].y});
+                ab += c[u];
+            }
         }
-        const double pml = key_value(s_prefix[r]);
-        const int64_t m = w->m_tail[r];
-        const double copies = (double)(m - (int64_t)above);
-        const double prod = __dmul_rn(copies, pml);
-        double total;
-        if (isfinite(prod) && isfinite(s.hi)) {
-            const double perr = fma(copies, pml, -prod);  // exact product error
-            dd_add(s, prod);
-            s.lo = __dadd_rn(s.lo, perr);
-            total = __dadd_rn(s.hi, s.lo);
-        } else {
-            total = __dadd_rn(__dadd_rn(s.hi, s.lo), prod);
+        dd_warp_reduce(s, ab);
+        if (lane == 0) {
+            const double pml = key_value(s_prefix[r]);
+            const int64_t m = prm.m_tail[r];
+            const double copies = (double)(m - (int64_t)ab);
+            const double prod = __dmul_rn(copies, pml);
+            double total;
+            if (isfinite(prod) && isfinite(s.hi)) {
+                const double perr = fma(copies, pml, -prod);  // exact product error
+                dd_add(s, prod);
+                s.lo = __dadd_rn(s.lo, perr);
+                total = __dadd_rn(s.hi, s.lo);
+            } else {
+                total = __dadd_rn(__dadd_rn(s.hi, s.lo), prod);
+            }
+            w->res[0][r] = pml;
+            w->res[1][r] = __ddiv_rn(total, (double)m);
         }
-        w->res[0][r] = pml;
-        w->res[1][r] = __ddiv_rn(total, (double)m);
     }
 }
 
@@ -216,13 +349,12 @@ int order_stat_k(int64_t n, double rp, int64_t *k) {
 }
 
 // Per-device cached K3 workspace (device K3Work + tail partials + pinned
-// host staging), serialised by a mutex.
+// result staging), serialised by a mutex.
 struct K3Cache {
     std::mutex mu;
-    int device = -1;
     K3Work *d_work = nullptr;
     TailPartial *d_part = nullptr;
-    K3Work *h_work = nullptr;  // pinned
+    double *h_res = nullptr;  // pinned [2][K3_GROUP]
     int grid = 0;
 };
 static K3Cache g_k3[64];
@@ -235,37 +367,38 @@ int k3_order_stats(const double *d_x, int64_t n, const double *rps, int64_t n_rp
     ARE_CUDA(cudaGetDevice(&dev));
     K3Cache &c = g_k3[dev & 63];
     std::lock_guard<std::mutex> guard(c.mu);
+    constexpr size_t smem = sizeof(unsigned int) * K3_GROUP * K3_BINS;
     if (!c.d_work) {
+        ARE_CUDA(cudaFuncSetAttribute(k3_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
-        ARE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_select, K3_THREADS, 0));
-        c.grid = sms * std::max(1, std::min(per_sm, 2));
+        ARE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_select, K3_THREADS, smem));
+        if (per_sm < 1) return fail(ARE_ECUDA, "K3 does not fit on an SM");
+        c.grid = sms * std::min(per_sm, 2);
         ARE_CUDA(cudaMalloc(&c.d_work, sizeof(K3Work)));
-        ARE_CUDA(cudaMalloc(&c.d_part, sizeof(TailPartial) * (size_t)c.grid * K3_MAX_RP));
-        ARE_CUDA(cudaHostAlloc(&c.h_work, sizeof(K3Work), cudaHostAllocDefault));
+        ARE_CUDA(cudaMalloc(&c.d_part, sizeof(TailPartial) * (size_t)c.grid * K3_GROUP));
+        ARE_CUDA(cudaHostAlloc(&c.h_res, sizeof(double) * 2 * K3_GROUP, cudaHostAllocDefault));
     }
-    for (int64_t base = 0; base < n_rp; base += K3_MAX_RP) {
-        const int R = (int)std::min<int64_t>(K3_MAX_RP, n_rp - base);
-        for (int r = 0; r < R; ++r) {
+    for (int64_t base = 0; base < n_rp; base += K3_GROUP) {
+        K3Params prm{};
+        prm.n_rp = (int)std::min<int64_t>(K3_GROUP, n_rp - base);
+        for (int r = 0; r < prm.n_rp; ++r) {
             int64_t k;
             int rc = order_stat_k(n, rps[base + r], &k);
             if (rc) return rc;
-            c.h_work->rank[r] = k;
-            c.h_work->m_tail[r] = n - k + 1;
+            prm.rank[r] = k;
+            prm.m_tail[r] = n - k + 1;
         }
-        std::memset(c.h_work->hist, 0, sizeof(c.h_work->hist));
-        c.h_work->bar_count = c.h_work->bar_gen = 0;
-        ARE_CUDA(cudaMemcpyAsync(c.d_work, c.h_work, offsetof(K3Work, res), cudaMemcpyHostToDevice, st));
+        ARE_CUDA(cudaMemsetAsync(c.d_work, 0, offsetof(K3Work, res), st));
         int grid = (int)std::min<int64_t>(c.grid, (n + K3_THREADS - 1) / K3_THREADS);
         grid = std::max(grid, 1);
-        int nn = R;
-        void *args[] = {(void *)&d_x, (void *)&n, (void *)&nn, (void *)&c.d_work, (void *)&c.d_part};
-        ARE_CUDA(cudaLaunchCooperativeKernel((void *)k3_select, grid, K3_THREADS, args, 0, st));
+        void *args[] = {(void *)&d_x, (void *)&n, (void *)&prm, (void *)&c.d_work, (void *)&c.d_part};
+        ARE_CUDA(cudaLaunchCooperativeKernel((void *)k3_select, grid, K3_THREADS, args, smem, st));
         ARE_LAUNCHED();
-        ARE_CUDA(cudaMemcpyAsync(c.h_work->res, c.d_work->res, sizeof(c.h_work->res), cudaMemcpyDeviceToHost, st));
+        ARE_CUDA(cudaMemcpyAsync(c.h_res, c.d_work->res, sizeof(double) * 2 * K3_GROUP, cudaMemcpyDeviceToHost, st));
         ARE_CUDA(cudaStreamSynchronize(st));
-        for (int r = 0; r < R; ++r) {
-            pml_out[base + r] = c.h_work->res[0][r];
-            tvar_out[base + r] = c.h_work->res[1][r];
+        for (int r = 0; r < prm.n_rp; ++r) {
+            pml_out[base + r] = c.h_res[r];
+            tvar_out[base + r] = c.h_res[K3_GROUP + r];
         }
     }
     return ARE_OK;
