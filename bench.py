@@ -350,6 +350,18 @@ def run_ours(args) -> None:
     e2e_s = time.perf_counter() - t_e2e
     e2e_s = max_over_ranks(e2e_s, dev) if world > 1 else e2e_s
     e2e_value = total_trials * e2e_steps / e2e_s
+    # the PCIe ceiling on this box: one plain pinned->device copy of the ids
+    d_probe = torch.empty(pinned.numel(), dtype=torch.int32, device=dev)
+    pcie = []
+    for _ in range(3):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(stream)
+        d_probe.copy_(pinned, non_blocking=True)
+        ev[1].record(stream)
+        torch.cuda.synchronize(dev)
+        pcie.append(pinned.numel() * 4 / (ev[0].elapsed_time(ev[1]) / 1e3) / 1e9)
+    del d_probe
+    pcie_gbs = max(pcie)
     n_local = t1 - t0
     h2d = int(yet.event_ids.nbytes + yet.offsets.nbytes + n_local * 8)  # ids, offsets, YLT to K3
     d2h = int(n_local * 8 + 2 * 8 * len(RPS))                        # YLT + pml/tvar
@@ -399,6 +411,9 @@ def run_ours(args) -> None:
         },
         "e2e": {"value": e2e_value, "unit": "trials/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3 / e2e_steps, "steps": e2e_steps,
+                "h2d_gbs": h2d / (e2e_s / e2e_steps) / 1e9,
+                "pcie_h2d_gbs_measured": pcie_gbs,
+                "frac_of_pcie": h2d / (e2e_s / e2e_steps) / 1e9 / pcie_gbs,
                 "path": "price_layer(pinned host YET) -> libaggrisk_b200 are_simulate_host -> order_stats"},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
