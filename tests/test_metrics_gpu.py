@@ -86,3 +86,39 @@ def test_rollup_bitwise(rng):
     assert portfolio_rollup(ylts[:1]) is ylts[0]
     with pytest.raises(ValueError):
         portfolio_rollup([])
+
+
+def _same(a: float, b: float) -> bool:
+    return (np.isnan(a) and np.isnan(b)) or a == b
+
+
+@pytest.mark.parametrize("case", ["tiny", "many_rps", "signed_zeros", "nan_tail", "uniform", "all_equal"])
+def test_k3_edge_cases(case, rng):
+    """Shapes the radix select treats specially: one/two trials, more return
+    periods than one launch holds (8) with duplicates sharing a prefix row,
+    -0.0 next to +0.0, NaN (sorted last, like np.partition), no ties."""
+    rps = [2.0, 10.0, 100.0, 250.0]
+    if case == "tiny":
+        x = np.array([3.0, 1.0])
+        rps = [2.0]
+    elif case == "many_rps":
+        x = rng.lognormal(5.0, 2.0, 50_000)
+        x[rng.random(x.size) < 0.2] = 1234.5
+        rps = [1.5, 2.0, 2.0, 3.0, 5.0, 10.0, 10.0, 20.0, 50.0, 100.0, 200.0, 250.0, 500.0, 1000.0,
+               2000.0, 5000.0, 10_000.0, 25_000.0, 50_000.0, 7.0]
+    elif case == "signed_zeros":
+        x = np.where(rng.random(10_000) < 0.5, -0.0, 0.0)
+        x[:100] = rng.random(100)
+    elif case == "nan_tail":
+        x = rng.random(10_000)
+        x[rng.choice(10_000, 30, replace=False)] = np.nan
+        rps = [2.0, 100.0, 1000.0, 5000.0]
+    elif case == "uniform":
+        x = rng.random(300_000) * 1e5
+    else:
+        x = np.full(70_000, 42.0)
+    p, t = order_stats(x, rps)
+    for r, pv, tv in zip(rps, p, t):
+        assert _same(pv, oracle.pml(x, r)), (r, pv, oracle.pml(x, r))
+        want = oracle.tvar(x, r)
+        assert (np.isnan(tv) and np.isnan(want)) or tv == pytest.approx(want, rel=1e-12, abs=1e-300)
