@@ -53,6 +53,26 @@ def bytes_per_trial(events: int = EVENTS, elts: int = N_ELTS) -> int:
     return 12 + 4 * events * (1 + elts)
 
 
+def host_descriptor() -> dict:
+    """Logical/physical core counts and CPU model (reference bench.py:79-96)."""
+    d = {"logical_cores": os.cpu_count(), "affinity_cores": host_cores(), "physical_cores": None, "cpu": None}
+    try:
+        import psutil
+
+        d["physical_cores"] = psutil.cpu_count(logical=False)
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    d["cpu"] = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return d
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -229,7 +249,7 @@ def run_reference_arm(args) -> None:
         "data": "synthetic", "impl": "reference",
         "config": {"workload": WORKLOAD, "sample_trials": sample, "events_per_trial": EVENTS,
                    "elts": N_ELTS, "catalog": CATALOG, "parallelism": f"{threads} host threads"},
-        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": dict({k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}, host=host_descriptor()),
         "e2e": {"value": res["value"], "unit": "trials/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -428,9 +448,15 @@ def run_ours(args) -> None:
         "setup_seconds": {"generate": gen_s},
     }
     if world == 1 and not args.no_cpu_baseline:
-        sample = args.cpu_sample or calibrate_sample(layer, host_cores(), 10.0)
-        cb = cpu_reference(layer, yet, sample, host_cores(), steps=1)
+        # min of 3 rounds, at W = all host cores and W = 1
+        cores = host_cores()
+        sample = args.cpu_sample or calibrate_sample(layer, cores, 4.0)
+        cb = cpu_reference(layer, yet, sample, cores, steps=3)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        sample1 = args.cpu_sample or calibrate_sample(layer, 1, 3.0)
+        cb1 = cpu_reference(layer, yet, sample1, 1, steps=3)
+        line["cpu_baseline"]["w1"] = {k: cb1[k] for k in ("value", "unit", "cores", "sample")}
+        line["cpu_baseline"]["host"] = host_descriptor()
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -7,7 +7,8 @@
       XL, terms from the generator), layers run back to back, then the
       on-device portfolio roll-up and K3 on it.
   C4  10M trials x 1000 events x 15 ELTs (40 GB of ids generated on the
-      device -- uniform ids, like the reference generator).
+      device -- uniform ids, like the reference generator), hot-set kernel
+      and the dense uncompacted kernel.
   C5  events/trial E in {100..5000} x ELTs J in {1..64}, T = 1e9 / E trials,
       catalog 2M: trials/s, K2 ms, algorithmic and compulsory GB/s.
 
@@ -103,8 +104,16 @@ def c4(quick: bool) -> dict:
     dyet = device_yet(trials, 1000, seed=44)
     terms = LayerTerms(500.0, 10_000.0, 140_000.0, 66_000.0)
     ms = time_k2(dyet, plan, terms, reps=3)
+    # also the dense, uncompacted layout (every lookup a
+    # float64 gather from the 240 MB tables: the exceeds-L2 regime)
+    dms = time_k2(dyet, plan, terms, reps=1, warm=1, variant="dense")
+    alg = trials * (12 + 4 * 1000 * 16)
     out = {"trials": trials, "events": 1000, "elts": 15, "k2_ms": ms, "trials_per_s": trials / (ms / 1e3),
-           "id_bytes": trials * 4000, "compulsory_frac": trials * 4016 / (ms / 1e3) / 1e9 / PEAK}
+           "id_bytes": trials * 4000, "compulsory_frac": trials * 4016 / (ms / 1e3) / 1e9 / PEAK,
+           "algorithmic_frac": alg / (ms / 1e3) / 1e9 / PEAK,
+           "dense": {"k2_ms": dms, "trials_per_s": trials / (dms / 1e3),
+                     "algorithmic_frac": alg / (dms / 1e3) / 1e9 / PEAK,
+                     "note": "k2_dense: the literal reference loop over dense float64 rows"}}
     print(json.dumps(out), flush=True)
     del dyet
     torch.cuda.empty_cache()
