@@ -45,6 +45,41 @@ def allgather_ylt(local, parts: list[tuple[int, int]], group=None):
     return torch.cat(chunks)
 
 
+def allgather_portfolio(local_layers, parts: list[tuple[int, int]], group=None):
+    """The C3 exchange: this rank first rolls its L layer
+    slices up into its portfolio slice -- the roll-up is per trial
+    (metrics.py:118-133), so it commutes with the trial sharding -- then ONE
+    all-gather moves the (L + 1)-row block.  Returns (the L full layer YLTs,
+    the full portfolio YLT), every one bit-identical to a single-GPU run."""
+    import torch
+    import torch.distributed as dist
+
+    layers = list(local_layers)
+    if not layers:
+        raise ValueError("no layer slices to gather")
+    n_layers, n = len(layers), int(layers[0].shape[0])
+    if n_layers == 1:
+        port = layers[0].clone()
+    elif layers[0].is_cuda:
+        from .risk import rollup_device
+
+        port = rollup_device(layers)
+    else:  # CPU tensors (gloo): the same left-to-right float64 sum
+        port = layers[0].clone()
+        for y in layers[1:]:
+            port = port + y
+    world = len(parts)
+    width = max(1, max(b - a for a, b in parts))
+    block = torch.zeros((n_layers + 1, width), dtype=torch.float64, device=layers[0].device)
+    if n:
+        block[:n_layers, :n] = torch.stack(layers)
+        block[n_layers, :n] = port
+    bufs = torch.empty((world, n_layers + 1, width), dtype=torch.float64, device=block.device)
+    dist.all_gather_into_tensor(bufs.view(-1), block.view(-1), group=group)
+    rows = [torch.cat([bufs[r, row, : b - a] for r, (a, b) in enumerate(parts)]) for row in range(n_layers + 1)]
+    return rows[:n_layers], rows[n_layers]
+
+
 def max_over_ranks(value: float, device=None, group=None) -> float:
     """Max of a host scalar over ranks (timings are reported as the slowest rank)."""
     import torch
