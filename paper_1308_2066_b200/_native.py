@@ -15,7 +15,9 @@ import numpy as np
 
 from .errors import EventOutOfRangeError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libaggrisk_b200.so")
+# ARE_LIB overrides the library path (kernel A/B experiments with alternative builds)
+LIB_PATH = os.environ.get("ARE_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                     "libaggrisk_b200.so")
 
 ARE_OK, ARE_EINVAL, ARE_ERANGE, ARE_ECUDA, ARE_ENOMEM, ARE_EINDEX = range(6)
 VARIANTS = {"auto": 0, "hotset": 1, "dense": 2}

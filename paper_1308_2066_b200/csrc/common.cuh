@@ -92,9 +92,10 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *p, uint64_t po
                  : "=r"(r) : "l"(p), "l"(policy));
     return r;
 }
-// Predicated streaming load: returns p[0] when rel < len, else 0 (no access).
-__device__ __forceinline__ uint32_t ld_stream_if(const uint32_t *p, uint32_t rel, uint32_t len, uint64_t policy) {
-    uint32_t r = 0;
+// Predicated streaming load: returns p[0] when rel < len, else `pad` (no access).
+__device__ __forceinline__ uint32_t ld_stream_if(const uint32_t *p, uint32_t rel, uint32_t len, uint64_t policy,
+                                                 uint32_t pad = 0) {
+    uint32_t r = pad;
     asm volatile(
         "{\n\t.reg .pred q;\n\t"
         "setp.lt.u32 q, %1, %2;\n\t"

@@ -8,9 +8,9 @@
 // and finally out[t] = clamp(c - agg_ret, 0, agg_lim).
 //
 // Hot-set kernel (k2_hotset): persistent, one CTA per SM, one warp per trial.
-//   * the trial's uint32 ids stream in with coalesced 16-byte loads
-//     (L1::no_allocate, L2 evict_first), one chunk of 128 occurrences per
-//     warp step (4 per lane, lane-major = trial order), next chunk prefetched;
+//   * the trial's uint32 ids stream in as coalesced 128-byte rows (one id per
+//     lane; L1::no_allocate, L2 evict_first), one chunk of 4 rows = 128
+//     occurrences per warp step, two chunks in flight;
 //   * a bit filter over event ids lives in shared memory (up to ~1.7M bits);
 //     events whose bit is clear are absent from every selected table and
 //     contribute exactly +-0, so they are
@@ -41,6 +41,22 @@ __device__ __forceinline__ uint32_t hot_hash(uint32_t e, uint32_t nbits) {
     if (HASH == 0) return e;
     if (HASH == 1) return min(e, e - nbits);
     return e % nbits;
+}
+
+// An event id whose filter bit is clear, used for the stream positions
+// outside a trial (they must not count as hits: event 0 shares its bit with
+// event nbits under HASH 1/2).  Searches the first 1024 bits; 0 if none
+// (then only speed suffers).  Warp-uniform result.
+__device__ __forceinline__ uint32_t cold_pad(const uint32_t *s_filter, int64_t filter_words, uint32_t nbits,
+                                             uint32_t row_len) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t w = lane < filter_words ? s_filter[lane] : 0xFFFFFFFFu;
+    const uint32_t lim = min(nbits, row_len);
+    uint32_t cand = 0xFFFFFFFFu;
+    if (~w) cand = (uint32_t)lane * 32 + (__ffs(~w) - 1);
+    if (cand >= lim) cand = 0xFFFFFFFFu;
+    cand = __reduce_min_sync(0xffffffffu, cand);
+    return cand == 0xFFFFFFFFu ? 0u : cand;
 }
 
 // Persistent hot-set kernel.  Each warp owns trials first + gw, first + gw +
@@ -83,6 +99,7 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
     const uint32_t *const ids = a.ids;
     const int64_t W = (int64_t)gridDim.x * NW;
     uint32_t emax = 0;  // largest id seen: ids > catalog are reported, not read
+    const uint32_t pad = cold_pad(s_filter, a.filter_words, nbits, a.row_len);
 
     // A batch is 32 queued events, one per lane.  It runs in two halves so
     // the record gathers of batch j are in flight while batch j-1 is finished
@@ -154,19 +171,18 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
         // for the in-flight load it copies): chunk s+2 loads while s is used
         uint32_t r0[4], r1[4], r2[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) r0[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream);
+        for (int k = 0; k < 4; ++k) r0[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream, pad);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) r1[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream);
+        for (int k = 0; k < 4; ++k) r1[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream, pad);
 
         auto step = [&](uint32_t (&cur)[4], uint32_t (&fut)[4]) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 256 + 32 * k, rel + 256 + 32 * k, len, pol_stream);
+            for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 256 + 32 * k, rel + 256 + 32 * k, len, pol_stream, pad);
             // filter words for all four rows first (independent shared loads)
             uint32_t ev[4], word[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                // out-of-trial lanes read 0: event 0 is never hot (slot 0
-                // unused; a plan with a loss there runs the dense kernel)
+                // out-of-trial lanes read `pad`, an id whose bit is clear
                 uint32_t e = cur[k];
                 if (CHECK) {
                     emax = max(emax, e);
