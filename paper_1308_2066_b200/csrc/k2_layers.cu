@@ -25,6 +25,7 @@ namespace are {
 
 static constexpr int LQCAP = 128;   // per-warp queue of event ids
 static constexpr int LSUB = 8;      // events per sub-batch
+static constexpr int LPL = K2L_MAX_LAYERS / 4;  // evaluation layers per lane
 
 template <int HASH>
 __device__ __forceinline__ uint32_t l_hash(uint32_t e, uint32_t nbits) {
@@ -93,7 +94,8 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
     uint64_t *s_mask = reinterpret_cast<uint64_t *>(smem + a.fin_bytes);  // per layer
     double *s_occ_ret = reinterpret_cast<double *>(s_mask + K2L_MAX_LAYERS);
     double *s_occ_lim = s_occ_ret + K2L_MAX_LAYERS;
-    double *s_occ = s_occ_lim + K2L_MAX_LAYERS;  // [NW][LSUB][K2L_MAX_LAYERS]
+    uint32_t *s_lbits = reinterpret_cast<uint32_t *>(s_occ_lim + K2L_MAX_LAYERS);  // [K2L_MAX_POOL]
+    double *s_occ = reinterpret_cast<double *>(s_lbits + K2L_MAX_POOL);  // [NW][LSUB][K2L_MAX_LAYERS]
     uint32_t *s_q = reinterpret_cast<uint32_t *>(s_occ + NW * LSUB * K2L_MAX_LAYERS);  // [NW][LQCAP]
     uint32_t *s_filter = s_q + NW * LQCAP;
 
@@ -102,6 +104,11 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
         s_mask[i] = L.masks[i];
         s_occ_ret[i] = L.terms[i].occ_ret;
         s_occ_lim[i] = L.terms[i].occ_lim;
+    }
+    for (int j = threadIdx.x; j < K2L_MAX_POOL; j += blockDim.x) {
+        uint32_t b = 0;
+        for (int l = 0; l < L.n_layers; ++l) b |= (uint32_t)((L.masks[l] >> j) & 1ull) << l;
+        s_lbits[j] = b;
     }
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(a.filter);
@@ -127,6 +134,14 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
     const double agg_ret = lane < nl ? L.terms[lane].agg_ret : 0.0;
     const double agg_lim = lane < nl ? L.terms[lane].agg_lim : 0.0;
     uint32_t emax = 0;
+    // this lane's evaluation layers sg, sg + 4, ... (constants in registers)
+    double lret[LPL], llim[LPL];
+#pragma unroll
+    for (int r = 0; r < LPL; ++r) {
+        const int l = sg + 4 * r;
+        lret[r] = l < nl ? s_occ_ret[l] : 0.0;
+        llim[r] = l < nl ? s_occ_lim[l] : 0.0;
+    }
 
     auto gather = [&](uint32_t qh, uint32_t n) -> Slot {
         Slot s{0.0, 0u, 0u};
@@ -134,9 +149,44 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
         return s;
     };
     // Evaluate a gathered sub-batch of n <= 8 events and fold it per layer.
+    // Fast path (warp-uniform): every event of the sub-batch sits in at most
+    // two pool tables (~99% of events at C3), so a layer's comb is
+    // 0.0 + [j0 in l] f0 + [j1 in l] f1 in pool order (an absent term adds
+    // +0.0 to a comb that is never -0: bit-identical to layer_eval).
     auto finish = [&](const Slot &s, uint32_t n, double &c) {
-        if ((uint32_t)si < n)
+        const uint32_t cnt = (uint32_t)si < n ? (s.meta >> 16) : 0u;
+        if (__all_sync(0xffffffffu, cnt <= 2u)) {
+            // the three possible combs (layer sees j0 only, j1 only, both)
+            // and, per entry, the layers that see it (bit 4r <-> layer sg + 4r)
+            double c10 = 0.0, c01 = 0.0, c11 = 0.0;
+            uint32_t m0 = 0, m1 = 0;
+            if (cnt) {
+                const uint32_t j0 = s.meta & 0xFFFFu;
+                c10 = __dadd_rn(0.0, fin_term(s_fin[j0], s.x));
+                c11 = c10;
+                m0 = s_lbits[j0] >> sg;
+            }
+            if (cnt == 2u) {
+                const Entry en = a.ovf[s.ovf];
+                const double f1 = fin_term(s_fin[en.j], en.x);
+                c01 = __dadd_rn(0.0, f1);
+                c11 = __dadd_rn(c10, f1);
+                m1 = s_lbits[en.j] >> sg;
+            }
+            double *o = occ + si * K2L_MAX_LAYERS;
+#pragma unroll
+            for (int r = 0; r < LPL; ++r) {
+                const int l = sg + 4 * r;
+                if (l < nl && (uint32_t)si < n) {
+                    const bool b0 = (m0 >> (4 * r)) & 1u, b1 = (m1 >> (4 * r)) & 1u;
+                    const double comb = b0 ? (b1 ? c11 : c10) : c01;
+                    const double v = clamp_ref(__dsub_rn(comb, lret[r]), llim[r]);
+                    o[l] = (b0 || b1) ? v : 0.0;
+                }
+            }
+        } else if ((uint32_t)si < n) {
             layer_eval(s, a.ovf, s_fin, s_mask, s_occ_ret, s_occ_lim, nl, sg, occ + si * K2L_MAX_LAYERS);
+        }
         __syncwarp();
         if (lane < nl)
             for (uint32_t i = 0; i < n; ++i) c = __dadd_rn(c, occ[i * K2L_MAX_LAYERS + lane]);
@@ -167,16 +217,18 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
         bool pending = false;  // a gathered sub-batch not yet evaluated
         Slot ps{0.0, 0u, 0u};
 
+        // three row buffers rotate by renaming (chunk ch + 2 loads while ch is
+        // filtered); the switch keeps one copy of the append/drain code
+        // (inlined once per call site, the drain would thrash the i-cache)
         uint32_t r0[4], r1[4], r2[4];
+        auto issue = [&](uint32_t (&fut)[4], int chn) {
+            const uint32_t *pc = p + ((int64_t)chn << 7);
+            const uint32_t rc = rel + ((uint32_t)chn << 7);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) r0[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) r1[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream);
-
-        auto step = [&](uint32_t (&cur)[4], uint32_t (&fut)[4]) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 256 + 32 * k, rel + 256 + 32 * k, len, pol_stream);
-            uint32_t ev[4], word[4];
+            for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(pc + 32 * k, rc + 32 * k, len, pol_stream);
+        };
+        auto filt = [&](const uint32_t (&cur)[4], uint32_t (&ev)[4], uint32_t (&hot)[4]) {
+            uint32_t word[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 uint32_t e = cur[k];
@@ -188,14 +240,29 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
                 word[k] = s_filter[l_hash<HASH>(e, nbits) >> 5];
             }
 #pragma unroll
+            for (int k = 0; k < 4; ++k) hot[k] = (word[k] >> (l_hash<HASH>(ev[k], nbits) & 31)) & 1u;
+        };
+        issue(r0, 0);
+        issue(r1, 1);
+        int phase = 0;
+        for (int ch = 0; ch < nchunks; ++ch) {
+            uint32_t ev[4], hot[4];
+            switch (phase) {
+                case 0: issue(r2, ch + 2); filt(r0, ev, hot); break;
+                case 1: issue(r0, ch + 2); filt(r1, ev, hot); break;
+                default: issue(r1, ch + 2); filt(r2, ev, hot); break;
+            }
+            phase = phase == 2 ? 0 : phase + 1;
+#pragma unroll 1
             for (int half = 0; half < 2; ++half) {
-#pragma unroll
-                for (int k = 2 * half; k < 2 * half + 2; ++k) {
-                    const bool hot = (word[k] >> (l_hash<HASH>(ev[k], nbits) & 31)) & 1u;
-                    const uint32_t b = ballot_full(hot);
-                    st_shared_if(q_saddr + (((qt + __popc(b & lt)) & (LQCAP - 1)) << 2), ev[k], hot);
-                    qt += __popc(b);
-                }
+                const uint32_t ea = half ? ev[2] : ev[0], eb = half ? ev[3] : ev[1];
+                const uint32_t ha = half ? hot[2] : hot[0], hb = half ? hot[3] : hot[1];
+                uint32_t b = ballot_full(ha);
+                st_shared_if(q_saddr + (((qt + __popc(b & lt)) & (LQCAP - 1)) << 2), ea, ha);
+                qt += __popc(b);
+                b = ballot_full(hb);
+                st_shared_if(q_saddr + (((qt + __popc(b & lt)) & (LQCAP - 1)) << 2), eb, hb);
+                qt += __popc(b);
                 __syncwarp();
                 while (qt - qh >= (uint32_t)LSUB) {
                     const Slot ns = gather(qh, LSUB);  // in flight while the previous one finishes
@@ -205,15 +272,6 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
                     qh += LSUB;
                 }
             }
-            p += 128;
-            rel += 128;
-        };
-        for (int ch = 0; ch < nchunks; ch += 3) {
-            step(r0, r2);
-            if (ch + 1 >= nchunks) break;
-            step(r1, r0);
-            if (ch + 2 >= nchunks) break;
-            step(r2, r1);
         }
         {
             const uint32_t n = qt - qh;
@@ -230,7 +288,7 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
 
 size_t k2_layers_fixed_smem(int n_sel) {
     constexpr int NW = K2L_THREADS / 32;
-    return (size_t)n_sel * sizeof(Fin) + 3 * K2L_MAX_LAYERS * sizeof(double) +
+    return (size_t)n_sel * sizeof(Fin) + 3 * K2L_MAX_LAYERS * sizeof(double) + K2L_MAX_POOL * sizeof(uint32_t) +
            (size_t)NW * LSUB * K2L_MAX_LAYERS * sizeof(double) +
            (size_t)NW * LQCAP * sizeof(uint32_t);
 }
