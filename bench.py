@@ -364,8 +364,10 @@ def run_ours(args) -> None:
     if world > 1:
         dist.barrier()
     t_e2e = time.perf_counter()
+    e2e_marks = [t_e2e]
     for _ in range(e2e_steps):
         e2e_step()
+        e2e_marks.append(time.perf_counter())
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t_e2e
     e2e_s = max_over_ranks(e2e_s, dev) if world > 1 else e2e_s
@@ -431,6 +433,10 @@ def run_ours(args) -> None:
         },
         "e2e": {"value": e2e_value, "unit": "trials/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3 / e2e_steps, "steps": e2e_steps,
+                "step_ms": [round((b - a) * 1e3, 2) for a, b in zip(e2e_marks, e2e_marks[1:])],
+                "median_step_ms": float(np.median(np.diff(e2e_marks))) * 1e3,
+                "note": "value = all steps over their total time; single steps on a shared host "
+                        "occasionally stall for 0.1-1 s (host memory / PCIe contention), see step_ms",
                 "h2d_gbs": h2d / (e2e_s / e2e_steps) / 1e9,
                 "pcie_h2d_gbs_measured": pcie_gbs,
                 "frac_of_pcie": h2d / (e2e_s / e2e_steps) / 1e9 / pcie_gbs,
@@ -468,7 +474,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
