@@ -412,6 +412,44 @@ def test_fused_layers_bitwise_equal_single_layer_runs():
         assert got.tobytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("n_layers", [2, 5, 7, 16])
+def test_fused_layers_dense_overlap_and_odd_layer_counts(n_layers):
+    """The fused kernel's fast path (events in <= 2 pool tables) and general
+    path (3+) mixed in one sub-batch: a dense 10-table pool (most hot events
+    sit in several tables), non-identity financial terms, layer counts that
+    are not multiples of 4; each layer bitwise equal to its own K2 run and
+    (first trials) to the reference loop."""
+    rng = np.random.default_rng(7000 + n_layers)
+    cat = 6_000
+    pool = []
+    for j in range(10):
+        ids = np.sort(rng.choice(np.arange(1, cat + 1), size=int(rng.integers(900, 2_400)), replace=False))
+        losses = rng.lognormal(0.0, 1.0, ids.shape[0]) * 1000.0
+        losses[rng.random(ids.shape[0]) < 0.05] = 0.0  # explicit zero losses
+        terms = FinancialTerms(float(rng.uniform(0.5, 2.0)), float(rng.uniform(0.0, 300.0)),
+                               float(rng.choice([math.inf, rng.uniform(500.0, 3000.0)])),
+                               float(rng.uniform(0.1, 1.0)))
+        pool.append(EventLossTable(cat, ids.astype(np.uint32), losses, terms))
+    layers = []
+    for i in range(n_layers):
+        sel = np.sort(rng.choice(10, size=int(rng.integers(2, 9)), replace=False))
+        occ_r, agg_r = float(rng.uniform(0, 800)), float(rng.uniform(0, 40_000))
+        terms = LayerTerms(occ_r, float(rng.choice([math.inf, rng.uniform(1000, 5000)])), agg_r,
+                           float(rng.choice([math.inf, rng.uniform(5_000, 60_000)])))
+        layers.append(Layer(f"L{i}", tuple(pool[j] for j in sel), terms))
+    yet = generate_yet(GeneratorSpec(seed=n_layers, catalog_size=cat, trial_count=1_500,
+                                     events_per_trial_range=(1, 400),
+                                     elt_size_range=(1, 10)), ids_only=True)
+    fused = run_aggregate_analysis(layers, yet)
+    for lay, y in zip(layers, fused):
+        single = run_aggregate_analysis([lay], yet)[0].losses
+        assert y.losses.tobytes() == single.tobytes(), lay.id
+    small = yet.head(200)
+    got = run_aggregate_analysis(layers, small)
+    for lay, y in zip(layers, got):
+        assert y.losses.tobytes() == _oracle_ylt(lay, small).tobytes(), lay.id
+
+
 # ------------------------------------------------- the C ABI drop-in itself --
 
 def test_c_abi_are_run_trials_matches_reference(instances):
