@@ -27,3 +27,7 @@ for e in map(int, args.es.split(",")):
                       "M_trials_per_s": round(t / ms / 1e3, 1)}), flush=True)
     del dyet
     torch.cuda.empty_cache()
+from paper_1308_2066_b200 import _native  # noqa: E402
+info = _native.plan_info(plan)
+print(json.dumps({"plan": {"hot_events": info.hot_events, "filter_bits": info.filter_bits,
+                           "smem_bytes": info.smem_bytes, "entries": info.entries}}))
