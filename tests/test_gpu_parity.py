@@ -268,6 +268,38 @@ def test_large_catalogs_use_wrapped_filter_exactly(catalog):
     assert np.count_nonzero(got) > 0
 
 
+@pytest.mark.parametrize("catalog", [50_000, 1_700_000, 3_000_000, 9_000_000])
+def test_kernel_instantiations_across_hash_modes(catalog):
+    """Every hot-set instantiation against the reference loop: filter hash
+    mode 0/1/2 (catalog below, within 2x, beyond 2x the shared-memory bits),
+    range-checked ids (price_layer: no validation) and validated ids (the
+    entry point), per-table and pre-combined records, and the fused layer
+    kernel on the same catalog."""
+    rng = np.random.default_rng(catalog + 1)
+    elts = []
+    for j in range(4):
+        ids = np.unique(rng.integers(1, catalog + 1, min(30_000, catalog // 3))).astype(np.uint32)
+        terms = FinancialTerms(float(rng.uniform(0.8, 1.5)), float(rng.uniform(0, 50)), float(rng.uniform(500, 4000)),
+                               float(rng.uniform(0.3, 1.0)))
+        elts.append(EventLossTable(catalog, ids, rng.lognormal(0, 1, ids.size) * 300.0, terms))
+    layer = Layer("L", tuple(elts), LayerTerms(30.0, 2_500.0, 800.0, 40_000.0))
+    hot = np.concatenate([e.event_ids for e in elts])
+    trials = [Trial.from_events(np.concatenate([rng.integers(1, catalog + 1, int(rng.integers(1, 600))),
+                                                rng.choice(hot, int(rng.integers(0, 60)))])) for _ in range(300)]
+    yet = YearEventTable.from_trials(trials, catalog)
+    want = _oracle_ylt(layer, yet)
+    assert np.count_nonzero(want) > 0
+    tset = TableSet.from_elts(elts, catalog)
+    for cfg in (HOT, EngineConfig(variant="hotset", precombine=True)):
+        got, _ = price_layer(yet, tset, None, layer.terms, cfg)
+        assert got.tobytes() == want.tobytes()
+        assert run_aggregate_analysis([layer], yet, cfg)[0].losses.tobytes() == want.tobytes()
+    second = Layer("M", tuple(elts[1:3]), LayerTerms(0.0, math.inf, 300.0, 20_000.0))
+    fused = run_aggregate_analysis([layer, second], yet)
+    assert fused[0].losses.tobytes() == want.tobytes()
+    assert fused[1].losses.tobytes() == _oracle_ylt(second, yet).tobytes()
+
+
 def test_256_tables_and_overflow_chains():
     cat = 300
     rng = np.random.default_rng(256)
