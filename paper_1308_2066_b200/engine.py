@@ -346,10 +346,35 @@ def price_layer(yet, tset: TableSet, selection: Sequence[int] | None, terms: Lay
     return out, _simulate(yet, tset, selection, terms, cfg, out)
 
 
+# Host YETs with at least this many occurrences enter the entry point through
+# HBM: ids + offsets are uploaded once, the YET half of validate_portfolio runs
+# on the device (K0, timestamps streamed through it), and every layer reads
+# the resident ids instead of re-streaming them over PCIe (SURVEY.md §8(f)
+# row 1).  Below it the host checks and the per-call stream are cheaper.
+PROMOTE_MIN_OCC = 1 << 24
+
+
+def _promote(yet):
+    if getattr(yet, "_device", None) is not None or callable(getattr(yet, "yet_violations", None)):
+        return yet
+    n = int(yet.offsets[-1]) if yet.offsets.size else 0
+    if n < PROMOTE_MIN_OCC or n == 0:
+        return yet
+    import torch
+
+    from .resident import DeviceYearEventTable
+
+    free, _ = torch.cuda.mem_get_info()
+    if 4 * n + 8 * int(yet.offsets.size) > free // 2:  # leave room for tables and outputs
+        return yet
+    return DeviceYearEventTable(yet)
+
+
 def run_aggregate_analysis_with_stats(layers: Sequence[Layer], yet, cfg: EngineConfig | None = None,
                                       pool=None) -> tuple[list[YearLossTable], RunStats]:
     """Validate, then per layer: K1 build (build_seconds), K2 (sim_seconds)."""
     cfg = cfg or EngineConfig()
+    yet = _promote(yet)
     violations = validate_portfolio(layers, yet)
     if violations:
         raise PortfolioInvalidError(violations)

@@ -96,3 +96,31 @@ def test_are1_straight_to_device_matches_host(tmp_path):
     save_yet(bad, tmp_path / "bad.are1")
     cats = [v.category for v in load_yet_device(tmp_path / "bad.are1").yet_violations()]
     assert "bad_timestamp" in cats
+
+
+@pytest.mark.parametrize("cases", ["", "range", "unsorted", "long unsorted zero_id", "nan"])
+def test_entry_point_promotes_large_host_yets(monkeypatch, cases):
+    """run_aggregate_analysis moves large host YETs into HBM (K0 validation,
+    resident ids): same violations (as the exception's report) and the same
+    bits as the host-validated, host-streamed path."""
+    import paper_1308_2066_b200.engine as engine
+    from paper_1308_2066_b200.engine import run_aggregate_analysis_with_stats
+
+    yet = _yet(cases)
+    layers = [_layer(), Layer("M", _layer().elts, LayerTerms(0.0, 70.0, 0.0, 300.0))]
+
+    def run():
+        try:
+            return run_aggregate_analysis_with_stats(layers, yet)
+        except PortfolioInvalidError as err:
+            return [str(v) for v in err.violations]
+
+    host = run()
+    monkeypatch.setattr(engine, "PROMOTE_MIN_OCC", 1)
+    dev = run()
+    if isinstance(host, list):
+        assert dev == host
+        return
+    (hy, hs), (dy, ds) = host, dev
+    assert [y.losses.tobytes() for y in dy] == [y.losses.tobytes() for y in hy]
+    assert (ds.trials, ds.layers, ds.lookups) == (hs.trials, hs.layers, hs.lookups)
