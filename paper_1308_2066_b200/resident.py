@@ -39,7 +39,10 @@ def _uploader():
     if _UPLOADER is None:
         from .h2d import Uploader
 
-        _UPLOADER = Uploader()
+        import os
+
+        # the staging copies are host-memory bound: use the cores we have
+        _UPLOADER = Uploader(threads=max(1, min(16, len(os.sched_getaffinity(0)))))
     return _UPLOADER
 
 
