@@ -257,6 +257,49 @@ def run_reference_arm(args) -> None:
 
 # ------------------------------------------------------------- our arm --
 
+def c3_fused(dyet, stream, reps: int = 5) -> dict:
+    """C3's portfolio shape on the resident YET: one fused K2 pass for 16
+    layers (K2-L), CUDA events on the launch stream."""
+    import math
+
+    import torch
+
+    from paper_1308_2066_b200.direct_access import TableSet
+    from paper_1308_2066_b200.engine import layer_pool, simulate_layers_device
+    from paper_1308_2066_b200.portfolio import Layer, LayerTerms
+    from paper_1308_2066_b200.synth import GeneratorSpec, generate_elt, generate_layer
+
+    spec = GeneratorSpec(seed=SEED, catalog_size=CATALOG, elt_count=32, elt_size_range=(10_000, 30_000),
+                         layer_count=16, elts_per_layer=15)
+    pool = [generate_elt(spec, i) for i in range(32)]
+    layers = []
+    for i in range(16):
+        g = generate_layer(spec, i, pool)
+        t = g.terms
+        terms = LayerTerms(t.occ_retention, t.occ_limit, 0.0, math.inf) if i % 2 == 0 else \
+            LayerTerms(0.0, math.inf, t.agg_retention, t.agg_limit)
+        layers.append(Layer(g.id, g.elts, terms))
+    pe, masks = layer_pool(layers)
+    ptset = TableSet.from_elts(pe, CATALOG)
+    lterms = [lay.terms for lay in layers]
+    out = torch.empty((16, dyet.trial_count), dtype=torch.float64, device=dyet.device)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            simulate_layers_device(dyet, ptset, masks, lterms, out=out)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(stream)
+        for _ in range(reps):
+            simulate_layers_device(dyet, ptset, masks, lterms, out=out)
+        ev[1].record(stream)
+    torch.cuda.synchronize(dyet.device)
+    ms = ev[0].elapsed_time(ev[1]) / reps
+    n = dyet.trial_count
+    return {"kernel_ms": ms, "layers": 16, "pool_elts": 32, "trials": n,
+            "portfolio_trials_per_s": n / (ms / 1e3), "layer_trials_per_s": 16 * n / (ms / 1e3),
+            "note": "C3 shape, one pass over the ids for 16 layers (k2_layers); per-layer YLTs bitwise "
+                    "equal to 16 single-layer K2 runs (tests); separately reported, not the headline"}
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -343,6 +386,11 @@ def run_ours(args) -> None:
     pe[1].record(stream)
     torch.cuda.synchronize(dev)
     pre_ms = pe[0].elapsed_time(pe[1]) / 10
+
+    # ---- separately reported work unit: C3's fused 16-layer pass (SURVEY 8(f)
+    # row 2) over this rank's resident ids: 16 layers from a 32-ELT pool,
+    # Per-Occurrence / Aggregate XL alternating (scripts/sweep.py c3)
+    c3 = c3_fused(dyet, stream)
 
     # ---- e2e: the public host API on pinned host buffers --------------------
     with GpuLocalCpus(local):
@@ -450,6 +498,7 @@ def run_ours(args) -> None:
                            "bytes_formula": "trials x (12 + 8*E) (one combined value per event)",
                            "achieved_gbs": (t1 - t0) * (12 + 8 * EVENTS) / (pre_ms / 1e3) / 1e9,
                            "note": "different unit of work (financial terms folded per event in K1); not the headline"},
+        "c3_fused_layers": c3,
         "pml": list(map(float, pml_v)), "tvar": list(map(float, tvar_v)),
         "setup_seconds": {"generate": gen_s},
     }
