@@ -54,6 +54,7 @@ typedef enum {
 
 typedef struct are_tables_s *are_tables_t;
 typedef struct are_plan_s *are_plan_t;
+typedef struct are_layer_table_s *are_layer_table_t;
 
 typedef struct {
     int64_t n_sel;            /* selected tables (accumulation order)            */
@@ -148,6 +149,22 @@ int are_simulate_layers_device(are_plan_t p, int32_t n_layers, const uint64_t *m
                                const int64_t *d_offsets, int64_t n_trials,
                                int64_t first, int64_t last,
                                double *d_out, int64_t out_stride, void *stream, int32_t flags);
+
+/* Pre-combined fused layers (SURVEY 8(f) rows 2 + 4; a separately reported
+ * work unit): are_layer_table_build evaluates, once per (pool plan, masks,
+ * layer terms), every hot event's occurrence value in every layer -- the
+ * float64 sequence of are_simulate_layers_device -- into a device table of
+ * 16 doubles per event id; are_simulate_layers_precombined then streams the
+ * ids and folds one table line per candidate event.  Bit-identical results.
+ * The plan must outlive the table.  Same arguments and errors as
+ * are_simulate_layers_device. */
+int are_layer_table_build(are_plan_t p, int32_t n_layers, const uint64_t *masks,
+                          const double *layer_terms, void *stream, are_layer_table_t *out);
+int are_layer_table_free(are_layer_table_t t);
+int are_simulate_layers_precombined(are_layer_table_t t, const uint32_t *d_event_ids, int64_t n_occ,
+                                    const int64_t *d_offsets, int64_t n_trials,
+                                    int64_t first, int64_t last,
+                                    double *d_out, int64_t out_stride, void *stream, int32_t flags);
 
 /* Host form: host ids/offsets/out; the library streams trial chunks to the
  * device (overlapping copies with K2) and returns when `out` is filled.

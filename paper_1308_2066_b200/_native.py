@@ -85,6 +85,10 @@ SIGNATURES = {
     "are_check_errors": (ctypes.c_int, [_P, _P]),
     "are_simulate_layers_device": (
         ctypes.c_int, [_P, _I32, _P, _P, _P, _I64, _P, _I64, _I64, _I64, _P, _I64, _P, _I32]),
+    "are_layer_table_build": (ctypes.c_int, [_P, _I32, _P, _P, _P, ctypes.POINTER(_P)]),
+    "are_layer_table_free": (ctypes.c_int, [_P]),
+    "are_simulate_layers_precombined": (
+        ctypes.c_int, [_P, _P, _I64, _P, _I64, _I64, _I64, _P, _I64, _P, _I32]),
     "are_simulate_host": (
         ctypes.c_int,
         [_P, _P, _I64, _P, _I64, _I64, _I64, _D, _D, _D, _D, _P, ctypes.POINTER(_I64), _I32],

@@ -536,34 +536,29 @@ int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ
     return k2_launch(a, v, di->sms, p->smem, (cudaStream_t)stream);
 }
 
-int are_simulate_layers_device(are_plan_t p, int32_t n_layers, const uint64_t *masks, const double *layer_terms,
-                               const uint32_t *d_event_ids, int64_t n_occ, const int64_t *d_offsets, int64_t n_trials,
-                               int64_t first, int64_t last, double *d_out, int64_t out_stride, void *stream,
-                               int32_t flags) {
+}  // extern "C"
+
+namespace are {
+// Checks shared by both fused-layer entry points; fills the per-layer terms.
+static int layer_terms_check(const are_plan_s *p, int32_t n_layers, const uint64_t *masks, const double *layer_terms,
+                             std::vector<LayerTerm> &lt) {
     if (!p) return fail(ARE_EINVAL, "null plan handle");
     if (!p->pool) return fail(ARE_EINVAL, "the fused layer kernel needs a pool plan (are_plan_build_pool)");
     if (n_layers < 1 || n_layers > K2L_MAX_LAYERS) return fail(ARE_EINVAL, "1..16 layers per fused launch");
-    if (first < 0 || last < first || last > n_trials) return fail(ARE_EINVAL, "trial range out of bounds");
     if (!(p->zero_skip && !p->slot0_hot)) return fail(ARE_EINVAL, "pool terms are not zero-exact; run layers singly");
     const uint64_t valid = p->n_sel >= 64 ? ~0ull : ((1ull << p->n_sel) - 1);
-    std::vector<LayerTerm> lt(n_layers);
+    lt.resize(n_layers);
     for (int l = 0; l < n_layers; ++l) {
         if (masks[l] & ~valid) return fail(ARE_EINDEX, "layer mask names a table outside the pool");
         lt[l] = LayerTerm{layer_terms[4 * l], layer_terms[4 * l + 1], layer_terms[4 * l + 2], layer_terms[4 * l + 3]};
         if (!occ_zero_ok(lt[l].occ_ret, lt[l].occ_lim))
             return fail(ARE_EINVAL, "layer occurrence terms are not zero-exact; run layers singly");
     }
-    DeviceInfo *di;
-    int rc;
-    if ((rc = use_device(p->device, &di))) return rc;
-    cudaStream_t st = (cudaStream_t)stream;
-    uint64_t *d_masks = nullptr;
-    LayerTerm *d_terms = nullptr;
-    ARE_CUDA(cudaMallocAsync((void **)&d_masks, sizeof(uint64_t) * n_layers, st));
-    ARE_CUDA(cudaMallocAsync((void **)&d_terms, sizeof(LayerTerm) * n_layers, st));
-    ARE_CUDA(cudaMemcpyAsync(d_masks, masks, sizeof(uint64_t) * n_layers, cudaMemcpyHostToDevice, st));
-    ARE_CUDA(cudaMemcpyAsync(d_terms, lt.data(), sizeof(LayerTerm) * n_layers, cudaMemcpyHostToDevice, st));
-    K2Args a{};
+    return ARE_OK;
+}
+
+static void layer_args(const are_plan_s *p, K2Args &a, const uint32_t *d_event_ids, int64_t n_occ,
+                       const int64_t *d_offsets, int64_t first, int64_t last, double *d_out) {
     a.ids = d_event_ids;
     a.id_base = 0;
     a.n_ids = n_occ;
@@ -575,11 +570,109 @@ int are_simulate_layers_device(are_plan_t p, int32_t n_layers, const uint64_t *m
     a.out_base = 0;
     a.err = p->d_err;
     fill_args(p, a, 0.0, 0.0, 0.0, 0.0);
+}
+}  // namespace are
+
+// A layer set's per-event occurrence table over one pool plan (pre-combined
+// fused layers).  The plan must outlive it.
+struct are_layer_table_s {
+    are_plan_s *plan = nullptr;
+    int32_t n_layers = 0;
+    uint64_t *d_masks = nullptr;
+    LayerTerm *d_terms = nullptr;
+    double *d_occ = nullptr;
+};
+
+extern "C" {
+
+int are_simulate_layers_device(are_plan_t p, int32_t n_layers, const uint64_t *masks, const double *layer_terms,
+                               const uint32_t *d_event_ids, int64_t n_occ, const int64_t *d_offsets, int64_t n_trials,
+                               int64_t first, int64_t last, double *d_out, int64_t out_stride, void *stream,
+                               int32_t flags) {
+    std::vector<LayerTerm> lt;
+    int rc;
+    if ((rc = layer_terms_check(p, n_layers, masks, layer_terms, lt))) return rc;
+    if (first < 0 || last < first || last > n_trials) return fail(ARE_EINVAL, "trial range out of bounds");
+    DeviceInfo *di;
+    if ((rc = use_device(p->device, &di))) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint64_t *d_masks = nullptr;
+    LayerTerm *d_terms = nullptr;
+    ARE_CUDA(cudaMallocAsync((void **)&d_masks, sizeof(uint64_t) * n_layers, st));
+    ARE_CUDA(cudaMallocAsync((void **)&d_terms, sizeof(LayerTerm) * n_layers, st));
+    ARE_CUDA(cudaMemcpyAsync(d_masks, masks, sizeof(uint64_t) * n_layers, cudaMemcpyHostToDevice, st));
+    ARE_CUDA(cudaMemcpyAsync(d_terms, lt.data(), sizeof(LayerTerm) * n_layers, cudaMemcpyHostToDevice, st));
+    K2Args a{};
+    layer_args(p, a, d_event_ids, n_occ, d_offsets, first, last, d_out);
     K2Layers L{n_layers, out_stride, d_masks, d_terms};
     rc = k2_layers_launch(a, L, !(flags & ARE_FLAG_IDS_VALIDATED), di->sms, p->smem, st);
     cudaFreeAsync(d_masks, st);
     cudaFreeAsync(d_terms, st);
     return rc;
+}
+
+int are_layer_table_build(are_plan_t p, int32_t n_layers, const uint64_t *masks, const double *layer_terms,
+                          void *stream, are_layer_table_t *out) {
+    if (!out) return fail(ARE_EINVAL, "null output handle");
+    *out = nullptr;
+    std::vector<LayerTerm> lt;
+    int rc;
+    if ((rc = layer_terms_check(p, n_layers, masks, layer_terms, lt))) return rc;
+    DeviceInfo *di;
+    if ((rc = use_device(p->device, &di))) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    auto *t = new are_layer_table_s();
+    t->plan = p;
+    t->n_layers = n_layers;
+    const int64_t row_len = p->tab->row_len;
+    cudaError_t e;
+    if ((e = cudaMalloc(&t->d_masks, sizeof(uint64_t) * n_layers)) != cudaSuccess ||
+        (e = cudaMalloc(&t->d_terms, sizeof(LayerTerm) * n_layers)) != cudaSuccess ||
+        (e = cudaMalloc(&t->d_occ, sizeof(double) * K2L_MAX_LAYERS * row_len)) != cudaSuccess) {
+        are_layer_table_free(t);
+        return cuda_fail(e, "allocate layer table");
+    }
+    if ((e = cudaMemcpyAsync(t->d_masks, masks, sizeof(uint64_t) * n_layers, cudaMemcpyHostToDevice, st)) !=
+            cudaSuccess ||
+        (e = cudaMemcpyAsync(t->d_terms, lt.data(), sizeof(LayerTerm) * n_layers, cudaMemcpyHostToDevice, st)) !=
+            cudaSuccess) {
+        are_layer_table_free(t);
+        return cuda_fail(e, "upload layer terms");
+    }
+    K2Args a{};
+    fill_args(p, a, 0.0, 0.0, 0.0, 0.0);
+    K2Layers L{n_layers, 0, t->d_masks, t->d_terms, nullptr};
+    if ((rc = k1_layer_occ_build(a, L, t->d_occ, di->sms, st)) ||
+        (rc = (cudaStreamSynchronize(st) == cudaSuccess ? ARE_OK : cuda_fail(cudaGetLastError(), "layer table")))) {
+        are_layer_table_free(t);
+        return rc;
+    }
+    *out = t;
+    return ARE_OK;
+}
+
+int are_layer_table_free(are_layer_table_t t) {
+    if (!t) return ARE_OK;
+    cudaFree(t->d_masks);
+    cudaFree(t->d_terms);
+    cudaFree(t->d_occ);
+    delete t;
+    return ARE_OK;
+}
+
+int are_simulate_layers_precombined(are_layer_table_t t, const uint32_t *d_event_ids, int64_t n_occ,
+                                    const int64_t *d_offsets, int64_t n_trials, int64_t first, int64_t last,
+                                    double *d_out, int64_t out_stride, void *stream, int32_t flags) {
+    if (!t) return fail(ARE_EINVAL, "null layer table handle");
+    if (first < 0 || last < first || last > n_trials) return fail(ARE_EINVAL, "trial range out of bounds");
+    are_plan_s *p = t->plan;
+    DeviceInfo *di;
+    int rc;
+    if ((rc = use_device(p->device, &di))) return rc;
+    K2Args a{};
+    layer_args(p, a, d_event_ids, n_occ, d_offsets, first, last, d_out);
+    K2Layers L{t->n_layers, out_stride, t->d_masks, t->d_terms, t->d_occ};
+    return k2_layers_pre_launch(a, L, !(flags & ARE_FLAG_IDS_VALIDATED), di->sms, (cudaStream_t)stream);
 }
 
 int are_check_errors(are_plan_t p, void *stream) {

@@ -128,6 +128,13 @@ __device__ __forceinline__ Slot ld_slot(const Slot *p, uint64_t policy) {
     return s;
 }
 
+// Read-only float64 gather with an L2 cache policy (resident tables).
+__device__ __forceinline__ double ld_nc_f64(const double *p, uint64_t policy) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(policy));
+    return v;
+}
+
 // Predicated 32-bit shared store (keeps queue appends branch-free).
 __device__ __forceinline__ void st_shared_if(uint32_t saddr, uint32_t v, bool pred) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}"

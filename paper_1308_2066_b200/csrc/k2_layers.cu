@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
     const uint32_t *const ids = a.ids;
     const int64_t W = (int64_t)gridDim.x * NW;
     const int nl = L.n_layers;
+    const uint32_t pad = cold_pad(s_filter, a.filter_words, nbits, a.row_len);  // out-of-trial lanes
     // this lane's fold layer (lane < nl)
     const double agg_ret = lane < nl ? L.terms[lane].agg_ret : 0.0;
     const double agg_lim = lane < nl ? L.terms[lane].agg_lim : 0.0;
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
             const uint32_t *pc = p + ((int64_t)chn << 7);
             const uint32_t rc = rel + ((uint32_t)chn << 7);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(pc + 32 * k, rc + 32 * k, len, pol_stream);
+            for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(pc + 32 * k, rc + 32 * k, len, pol_stream, pad);
         };
         auto filt = [&](const uint32_t (&cur)[4], uint32_t (&ev)[4], uint32_t (&hot)[4]) {
             uint32_t word[4];

@@ -43,22 +43,6 @@ __device__ __forceinline__ uint32_t hot_hash(uint32_t e, uint32_t nbits) {
     return e % nbits;
 }
 
-// An event id whose filter bit is clear, used for the stream positions
-// outside a trial (they must not count as hits: event 0 shares its bit with
-// event nbits under HASH 1/2).  Searches the first 1024 bits; 0 if none
-// (then only speed suffers).  Warp-uniform result.
-__device__ __forceinline__ uint32_t cold_pad(const uint32_t *s_filter, int64_t filter_words, uint32_t nbits,
-                                             uint32_t row_len) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t w = lane < filter_words ? s_filter[lane] : 0xFFFFFFFFu;
-    const uint32_t lim = min(nbits, row_len);
-    uint32_t cand = 0xFFFFFFFFu;
-    if (~w) cand = (uint32_t)lane * 32 + (__ffs(~w) - 1);
-    if (cand >= lim) cand = 0xFFFFFFFFu;
-    cand = __reduce_min_sync(0xffffffffu, cand);
-    return cand == 0xFFFFFFFFu ? 0u : cand;
-}
-
 // Persistent hot-set kernel.  Each warp owns trials first + gw, first + gw +
 // W, ...; a trial's ids are read as 32-id coalesced rows (row k of a 128-id
 // chunk is ids [base + 32k, base + 32k + 32), lane l takes one id), two chunks
@@ -301,7 +285,8 @@ int k2_prepare(int device) {
     (void)device;
     int rc;
     if ((rc = prepare_pre<false>()) || (rc = prepare_pre<true>())) return rc;
-    return k2_layers_prepare();
+    if ((rc = k2_layers_prepare())) return rc;
+    return k2_layers_pre_prepare();
 }
 
 template <bool PRE>

@@ -52,7 +52,24 @@ struct K2Layers {
     int64_t out_stride;      // out[l * out_stride + t]
     const uint64_t *masks;   // pool-row bitmask per layer
     const LayerTerm *terms;  // per layer
+    const double *occ_table = nullptr;  // pre-combined: occ[e * 16 + l] (k1_layer_occ)
 };
+
+// An event id whose filter bit is clear, used for the stream positions
+// outside a trial (they must not count as hits: event 0 shares its bit with
+// event nbits under HASH 1/2).  Searches the first 1024 bits; 0 if none
+// (then only speed suffers).  Warp-uniform result.
+__device__ __forceinline__ uint32_t cold_pad(const uint32_t *s_filter, int64_t filter_words, uint32_t nbits,
+                                             uint32_t row_len) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t w = lane < filter_words ? s_filter[lane] : 0xFFFFFFFFu;
+    const uint32_t lim = min(nbits, row_len);
+    uint32_t cand = 0xFFFFFFFFu;
+    if (~w) cand = (uint32_t)lane * 32 + (__ffs(~w) - 1);
+    if (cand >= lim) cand = 0xFFFFFFFFu;
+    cand = __reduce_min_sync(0xffffffffu, cand);
+    return cand == 0xFFFFFFFFu ? 0u : cand;
+}
 
 // Largest dynamic shared-memory carve-out requested by K2 (sm_100: 227 KB).
 inline int k2_max_dynamic_smem() { return 227 * 1024; }
@@ -62,5 +79,9 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
 size_t k2_layers_fixed_smem(int n_sel);
 int k2_layers_prepare();
 int k2_layers_launch(const K2Args &a, const K2Layers &L, bool check, int sms, size_t smem_bytes, cudaStream_t st);
+// pre-combined fused layers (k2_layers_pre.cu)
+int k1_layer_occ_build(const K2Args &a, const K2Layers &L, double *d_occ, int sms, cudaStream_t st);
+int k2_layers_pre_prepare();
+int k2_layers_pre_launch(const K2Args &a, const K2Layers &L, bool check, int sms, cudaStream_t st);
 
 }  // namespace are

@@ -295,8 +295,31 @@ def layer_pool(layers: Sequence[Layer]):
     return [pool[i] for i in order], masks
 
 
-def simulate_layers_device(dyet, pool_tset: TableSet, masks, terms_list, out=None, variant_flags: int = 0):
-    """Fused K2 over a DeviceYearEventTable: (L, T) float64 CUDA tensor of YLTs."""
+_LAYER_TABLES: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _layer_table(plan, masks: np.ndarray, lt: np.ndarray, stream) -> _native.Handle:
+    """Pre-combined occurrence table of one layer group (K1-L), cached per
+    (pool plan, masks, layer terms)."""
+    per_plan = _LAYER_TABLES.setdefault(plan, {})
+    key = (masks.tobytes(), lt.tobytes())
+    hit = per_plan.get(key)
+    if hit is None:
+        h = _native._P()
+        _native.check(_native.load().are_layer_table_build(
+            plan.value, masks.shape[0], masks.ctypes.data, lt.ctypes.data, _native.ctypes.c_void_p(stream),
+            _native.ctypes.byref(h)))
+        hit = per_plan[key] = _native.Handle(h.value, "are_layer_table_free")
+    return hit
+
+
+def simulate_layers_device(dyet, pool_tset: TableSet, masks, terms_list, out=None, variant_flags: int = 0,
+                           precombine: bool = False):
+    """Fused K2 over a DeviceYearEventTable: (L, T) float64 CUDA tensor of YLTs.
+    `precombine` runs the pre-combined variant (SURVEY 8(f) rows 2 + 4): each
+    hot event's per-layer occurrence value is evaluated once (K1-L) and K2
+    folds one table line per candidate event; bit-identical results, a
+    separately reported work unit."""
     import torch
 
     n = dyet.trial_count
@@ -310,16 +333,22 @@ def simulate_layers_device(dyet, pool_tset: TableSet, masks, terms_list, out=Non
         m = np.ascontiguousarray(masks[g:g + MAX_FUSED_LAYERS], dtype=np.uint64)
         lt = np.ascontiguousarray([[t.occ_retention, t.occ_limit, t.agg_retention, t.agg_limit]
                                    for t in terms_list[g:g + MAX_FUSED_LAYERS]], dtype=np.float64)
-        _native.check(lib.are_simulate_layers_device(
-            plan.value, m.shape[0], m.ctypes.data, lt.ctypes.data, dyet.d_ids.data_ptr(), dyet._n_ids,
-            dyet.d_offsets.data_ptr(), n, 0, n, out[g].data_ptr(), n, _native.ctypes.c_void_p(st.cuda_stream),
-            flags))
+        if precombine:
+            table = _layer_table(plan, m, lt, st.cuda_stream)
+            _native.check(lib.are_simulate_layers_precombined(
+                table.value, dyet.d_ids.data_ptr(), dyet._n_ids, dyet.d_offsets.data_ptr(), n, 0, n,
+                out[g].data_ptr(), n, _native.ctypes.c_void_p(st.cuda_stream), flags))
+        else:
+            _native.check(lib.are_simulate_layers_device(
+                plan.value, m.shape[0], m.ctypes.data, lt.ctypes.data, dyet.d_ids.data_ptr(), dyet._n_ids,
+                dyet.d_offsets.data_ptr(), n, 0, n, out[g].data_ptr(), n, _native.ctypes.c_void_p(st.cuda_stream),
+                flags))
     _native.check(lib.are_check_errors(plan.value, _native.ctypes.c_void_p(st.cuda_stream)))
     return out
 
 
 def _fusable(layers: Sequence[Layer], cfg: EngineConfig):
-    if len(layers) < 2 or cfg.variant not in ("auto", "hotset") or cfg.precombine:
+    if len(layers) < 2 or cfg.variant not in ("auto", "hotset"):
         return None
     got = layer_pool(layers)
     if got is None:
@@ -395,7 +424,7 @@ def run_aggregate_analysis_with_stats(layers: Sequence[Layer], yet, cfg: EngineC
         dyet = yet if getattr(yet, "_device", None) is not None else DeviceYearEventTable(yet)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        d = simulate_layers_device(dyet, tset, masks, [layer.terms for layer in layers])
+        d = simulate_layers_device(dyet, tset, masks, [layer.terms for layer in layers], precombine=cfg.precombine)
         host = d.cpu().numpy()
         stats.sim_seconds += time.perf_counter() - t0
         occ = int(yet.offsets[-1])

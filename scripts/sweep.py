@@ -177,12 +177,29 @@ def c3(quick: bool) -> dict:
     b.record()
     torch.cuda.synchronize()
     fms = a.elapsed_time(b) / reps
+
+    def pre_step():  # per-event occurrence table (SURVEY 8(f) rows 2 + 4)
+        simulate_layers_device(dyet, ptset, masks, [l.terms for l in layers], out=fused, precombine=True)
+        total = rollup_device([fused[i] for i in range(16)])
+        return order_stats(total, [10.0, 50.0, 100.0, 250.0])
+
+    for _ in range(2):
+        pre_step()
+    pre_same = all(torch.equal(fused[i], outs[i]) for i in range(16))
+    a.record()
+    for _ in range(reps):
+        pre_step()
+    b.record()
+    torch.cuda.synchronize()
+    pms = a.elapsed_time(b) / reps
     out = {"trials": trials, "layers": 16, "step_ms": ms, "trials_per_s": trials / (ms / 1e3),
            "layer_trials_per_s": 16 * trials / (ms / 1e3), "portfolio_pml": list(map(float, res[0])),
            "note": "16 K2 launches (one per layer) + k3_rollup + K3 per step; unfused",
            "fused_step_ms": fms, "fused_trials_per_s": trials / (fms / 1e3),
            "fused_layer_trials_per_s": 16 * trials / (fms / 1e3), "fused_bitwise_equal_unfused": bool(same),
-           "fused_portfolio_pml": list(map(float, fres[0]))}
+           "fused_portfolio_pml": list(map(float, fres[0])),
+           "precombined_step_ms": pms, "precombined_layer_trials_per_s": 16 * trials / (pms / 1e3),
+           "precombined_bitwise_equal_unfused": bool(pre_same)}
     print(json.dumps(out), flush=True)
     return out
 

@@ -21,7 +21,13 @@ def main() -> None:
                 f"-> {c['fused_trials_per_s'] / 1e6:.1f} M portfolio-trials/s, "
                 f"{c['fused_layer_trials_per_s'] / 1e6:.0f} M layer-trials/s; every layer's YLT bitwise equal to the "
                 f"unfused run: {c['fused_bitwise_equal_unfused']}",
-                f"- portfolio PML at rp 10/50/100/250: {', '.join(f'{x:,.0f}' for x in c['fused_portfolio_pml'])}", ""]
+                f"- portfolio PML at rp 10/50/100/250: {', '.join(f'{x:,.0f}' for x in c['fused_portfolio_pml'])}"]
+        if "precombined_step_ms" in c:
+            out += [f"- pre-combined fused pass (per-event table of the 16 occurrence values, K1-L; a separately "
+                    f"reported work unit) + roll-up + K3: {c['precombined_step_ms']:.2f} ms -> "
+                    f"{c['precombined_layer_trials_per_s'] / 1e6:.0f} M layer-trials/s; bitwise equal: "
+                    f"{c['precombined_bitwise_equal_unfused']}"]
+        out += [""]
     if "c4" in d:
         c = d["c4"]
         out += [f"## C4 -- {c['trials']:,} trials x {c['events']} events x {c['elts']} ELTs "

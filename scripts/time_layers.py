@@ -29,14 +29,18 @@ pe, masks = layer_pool(layers)
 ts = TableSet.from_elts(pe, CATALOG)
 dyet = device_yet(args.trials, 1000, 33)
 out = torch.empty((16, args.trials), dtype=torch.float64, device="cuda")
-for _ in range(2):
-    simulate_layers_device(dyet, ts, masks, [l.terms for l in layers], out=out)
-torch.cuda.synchronize()
-a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-a.record()
-for _ in range(args.reps):
-    simulate_layers_device(dyet, ts, masks, [l.terms for l in layers], out=out)
-b.record()
-torch.cuda.synchronize()
-print(f"fused 16-layer K2: {a.elapsed_time(b) / args.reps:.3f} ms per {args.trials} trials "
-      f"({os.environ.get('ARE_LIB', 'default build')})")
+res = {}
+for pre in (False, True):
+    for _ in range(2):
+        simulate_layers_device(dyet, ts, masks, [l.terms for l in layers], out=out, precombine=pre)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.reps):
+        simulate_layers_device(dyet, ts, masks, [l.terms for l in layers], out=out, precombine=pre)
+    b.record()
+    torch.cuda.synchronize()
+    res[pre] = out.clone()
+    print(f"fused 16-layer K2{' pre-combined' if pre else ''}: {a.elapsed_time(b) / args.reps:.3f} ms per "
+          f"{args.trials} trials ({os.environ.get('ARE_LIB', 'default build')})")
+print("bitwise equal:", bool(torch.equal(res[False], res[True])))

@@ -480,6 +480,21 @@ def test_fused_layers_dense_overlap_and_odd_layer_counts(n_layers):
     got = run_aggregate_analysis(layers, small)
     for lay, y in zip(layers, got):
         assert y.losses.tobytes() == _oracle_ylt(lay, small).tobytes(), lay.id
+    # pre-combined variant (per-event occurrence table, K1-L): same bits
+    from paper_1308_2066_b200.engine import layer_pool, simulate_layers_device
+    from paper_1308_2066_b200.resident import DeviceYearEventTable
+
+    pool_elts, masks = layer_pool(layers)
+    ptset = TableSet.from_elts(pool_elts, cat)
+    dyet = DeviceYearEventTable(yet)
+    terms = [lay.terms for lay in layers]
+    exact = simulate_layers_device(dyet, ptset, masks, terms).cpu().numpy()
+    for _ in range(2):  # second call reuses the cached table
+        pre = simulate_layers_device(dyet, ptset, masks, terms, precombine=True).cpu().numpy()
+        assert pre.tobytes() == exact.tobytes()
+    assert all(exact[i].tobytes() == fused[i].losses.tobytes() for i in range(n_layers))
+    via_entry = run_aggregate_analysis(layers, yet, EngineConfig(precombine=True))
+    assert all(y.losses.tobytes() == fused[i].losses.tobytes() for i, y in enumerate(via_entry))
 
 
 # ------------------------------------------------- the C ABI drop-in itself --
