@@ -16,8 +16,11 @@ ncu --set full --clock-control none --import-source on -k regex:k2_hotset -s 1 -
     python scripts/profile_k2.py --launches 2 > gpurun_out/ncu_k2_$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k3_select -s 2 -c 1 -o gpurun_out/k3_$TAG \
     python scripts/profile_k2.py --launches 3 --k3 > gpurun_out/ncu_k3_$TAG.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k2_layers -s 1 -c 1 -o gpurun_out/k2l_$TAG \
+ncu --set full --clock-control none --import-source on -k regex:"^k2_layers$" -s 1 -c 1 -o gpurun_out/k2l_$TAG \
     python scripts/profile_layers.py > gpurun_out/ncu_k2l_$TAG.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"^k2_layers_pre$" -s 1 -c 1 -o gpurun_out/k2lp_$TAG \
+    python scripts/time_layers.py --trials 200000 --reps 1 > gpurun_out/ncu_k2lp_$TAG.log 2>&1
+timeout 600 python scripts/entry_e2e.py > gpurun_out/entry_e2e_$TAG.json 2> gpurun_out/entry_e2e_$TAG.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_under_ncu_$TAG.log 2>&1
 timeout 1500 python scripts/sweep.py --out gpurun_out/sweep_$TAG.json > gpurun_out/sweep_$TAG.log 2>&1; tail -2 gpurun_out/sweep_$TAG.log
