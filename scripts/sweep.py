@@ -231,6 +231,76 @@ def validate(quick: bool) -> dict:
     return out
 
 
+# The reference's own linear-scaling sweeps (pkg/src/aggrisk/bench.py:159-230,
+# base spec :177-184; asserted by tests/test_acceptance.py:121-137) with the
+# seconds its recorded run reports for its compiled CPU engine, one worker
+# (pkg/test_output.txt:244-253).
+REF_RECORDED = {
+    "trials": {20_000: 0.225, 40_000: 0.466, 60_000: 0.712, 80_000: 0.963, 100_000: 1.201},
+    "events_per_trial": {800: 1.132, 900: 1.249, 1000: 1.457, 1100: 1.547, 1200: 1.774},
+    "elts_per_layer": {3: 0.118, 6: 0.240, 9: 0.382, 12: 0.518, 15: 0.685},
+    "layers": {1: 0.114, 2: 0.228, 3: 0.346, 4: 0.441, 5: 0.573},
+}
+
+
+def refsweeps(quick: bool) -> dict:
+    """The same four sweeps through the same API (run_aggregate_analysis_with_
+    stats, RunStats.sim_seconds, min over 3 interleaved rounds), inputs from
+    the reference generator restatement (byte-identical YET/ELTs)."""
+    from paper_1308_2066_b200.engine import run_aggregate_analysis_with_stats
+    from paper_1308_2066_b200.synth import generate_yet
+
+    base = dict(seed=7, catalog_size=50_000, trial_count=20_000, events_per_trial_range=(1000, 1000),
+                elt_count=15, elt_size_range=(10_000, 30_000))
+
+    def flat(elts, lid="bench"):
+        return Layer(lid, tuple(elts), LayerTerms())
+
+    plans = {}
+    spec = GeneratorSpec(**{**base, "trial_count": 100_000, "elt_count": 6})
+    yet = generate_yet(spec)
+    elts = [generate_elt(spec, i) for i in range(6)]
+    plans["trials"] = [(v, [flat(elts)], yet.head(v)) for v in REF_RECORDED["trials"]]
+    spec = GeneratorSpec(**{**base, "events_per_trial_range": (1200, 1200), "trial_count": 40_000})
+    full = generate_yet(spec)
+    elts = [generate_elt(spec, i) for i in range(15)]
+    ev = full.event_ids.reshape(-1, 1200)
+    ts = full.timestamps.reshape(-1, 1200)
+    from paper_1308_2066_b200.portfolio import YearEventTable
+
+    plans["events_per_trial"] = [
+        (v, [flat(elts)], YearEventTable(full.catalog_size, np.ascontiguousarray(ev[:, :v]).ravel(),
+                                         np.ascontiguousarray(ts[:, :v]).ravel(),
+                                         np.arange(ev.shape[0] + 1, dtype=np.int64) * v))
+        for v in REF_RECORDED["events_per_trial"]]
+    spec = GeneratorSpec(**base)
+    yet = generate_yet(spec)
+    elts = [generate_elt(spec, i) for i in range(15)]
+    plans["elts_per_layer"] = [(v, [flat(elts[:v])], yet) for v in REF_RECORDED["elts_per_layer"]]
+    spec = GeneratorSpec(**{**base, "elt_count": 3})
+    yet = generate_yet(spec)
+    elts = [generate_elt(spec, i) for i in range(3)]
+    plans["layers"] = [(v, [flat(elts, f"bench-{i}") for i in range(v)], yet) for v in REF_RECORDED["layers"]]
+
+    out = {}
+    for name, plan in plans.items():
+        best = {}
+        for _ in range(3):  # interleaved rounds, minimum per point (reference bench.py:113-140)
+            for v, layers, y in plan:
+                _, st = run_aggregate_analysis_with_stats(layers, y)
+                best[v] = min(best.get(v, math.inf), st.sim_seconds)
+        xs = np.array(sorted(best), dtype=np.float64)
+        ys = np.array([best[v] for v in sorted(best)])
+        fit = np.polyfit(xs, ys, 1)
+        r2 = 1.0 - float(np.sum((ys - np.polyval(fit, xs)) ** 2) / np.sum((ys - ys.mean()) ** 2))
+        out[name] = {"points": [{"value": int(v), "sim_seconds": best[v],
+                                 "reference_recorded_seconds": REF_RECORDED[name][v],
+                                 "speedup": REF_RECORDED[name][v] / best[v]} for v in sorted(best)],
+                     "r2": r2}
+        print(json.dumps({name: out[name]}), flush=True)
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")

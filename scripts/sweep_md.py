@@ -50,6 +50,18 @@ def main() -> None:
                        f"| {r['hot_events']:,} | {r['algorithmic_gbs']:.0f} ({r['algorithmic_frac']:.2f}) "
                        f"| {r['compulsory_gbs']:.0f} ({r['compulsory_frac']:.2f}) |")
         out += [""]
+    if "refsweeps" in d:
+        out += ["## The reference's own linear-scaling sweeps (catalog 50k, 1000 events, identity terms)", "",
+                "Same entry point and counter as the reference bench (`run_aggregate_analysis_with_stats`, "
+                "`RunStats.sim_seconds`, min of 3 interleaved rounds); reference = its recorded run of the compiled "
+                "CPU engine on one worker (`pkg/test_output.txt:244-253`).", "",
+                "| sweep | point | reference s | this engine ms | speed-up |", "|---|---|---|---|---|"]
+        for name, r in d["refsweeps"].items():
+            for p in r["points"]:
+                out.append(f"| {name} | {p['value']:,} | {p['reference_recorded_seconds']:.3f} | "
+                           f"{p['sim_seconds'] * 1e3:.2f} | {p['speedup']:,.0f}x |")
+            out.append(f"| {name} | R^2 of this engine's times | | {r['r2']:.4f} | |")
+        out += [""]
     open(dst, "w").write("\n".join(out))
 
 
