@@ -19,6 +19,13 @@
 // and evaluates layers g, g+4, g+8, ... for it, writing occ[i][l] to shared
 // memory; then lane l (< L) folds occ[0..n)[l] into its own register c_l.  The
 // fold is therefore lane-parallel across layers instead of warp-redundant.
+// When every event of a sub-batch sits in at most two pool tables (~99% at
+// C3) a warp-uniform fast path replaces the general per-layer loop: per pool
+// table a word of the layers that contain it, the event's three possible
+// combs (first table only, second only, both -- in pool order), layer terms
+// in registers.  The row buffers rotate through a phase switch so the append
+// and drain code (which inlines the evaluation) exists once: six inlined
+// copies thrashed the instruction cache.
 #include "k2_trials.cuh"
 
 namespace are {
