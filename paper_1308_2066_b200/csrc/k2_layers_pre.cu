@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers_pre(const K2Args a, 
     // for p = 0..15 (events past n read event 0's line: all zero)
     auto gather = [&](uint32_t qh, uint32_t n, double (&v)[16]) {
         const uint32_t mine = (uint32_t)lane < n ? q[(qh + lane) & (PQCAP - 1)] : 0u;
+        __syncwarp();  // the ring slot may be rewritten by another lane later
 #pragma unroll
         for (int p = 0; p < 16; ++p) {
             const uint32_t e = __shfl_sync(0xffffffffu, mine, 2 * p + half);
