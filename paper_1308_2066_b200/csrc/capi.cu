@@ -91,6 +91,12 @@ struct are_plan_s {
     bool precombined = false;
     unsigned int *d_err = nullptr;
     size_t smem = 0;
+    // event-major copy of the selected rows for the dense kernel (built on
+    // its first use; n_sel <= EM_MAX_SEL)
+    std::mutex em_mu;
+    double *d_em = nullptr;
+    int32_t em_stride = 0;
+    bool em_tried = false;
 };
 
 static void tables_release(are_tables_s *t) {
@@ -208,6 +214,37 @@ static int choose_variant(const are_plan_s *p, double occ_ret, double occ_lim, i
     return ARE_OK;
 }
 
+// The dense kernel's event-major table: built once per plan on first use,
+// only when the selected rows exceed what L2 keeps (measured: catalog 2M x 15
+// rows, 240 MB: 7.1 vs 19.1 ms per 100k trials; 200k x 15 rows, 24 MB, stays
+// L2-resident and the row-major walk wins, 5.4 vs 7.1 ms).  If it cannot be
+// allocated the row-major dense kernel runs instead.
+static constexpr int64_t EM_MAX_SEL = 32;
+static constexpr int64_t EM_MIN_BYTES = 64ll << 20;
+static int ensure_event_major(are_plan_s *p, int sms, cudaStream_t st) {
+    std::lock_guard<std::mutex> g(p->em_mu);
+    if (p->em_tried) return ARE_OK;
+    p->em_tried = true;
+    if (p->n_sel > EM_MAX_SEL || p->n_sel * p->tab->row_len * (int64_t)sizeof(double) < EM_MIN_BYTES) return ARE_OK;
+    const int stride = (int)((p->n_sel + 1) & ~1);
+    const size_t bytes = (size_t)p->tab->row_len * stride * sizeof(double);
+    double *d = nullptr;
+    if (cudaMalloc(&d, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return ARE_OK;
+    }
+    int rc = k1_event_major(p->tab->d, p->tab->row_len, p->d_rows, (int)p->n_sel, stride, d, sms, st);
+    // other streams may use the plan next: the table must be complete
+    if (rc == ARE_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "event-major table");
+    if (rc) {
+        cudaFree(d);
+        return rc;
+    }
+    p->d_em = d;
+    p->em_stride = stride;
+    return ARE_OK;
+}
+
 static void fill_args(const are_plan_s *p, K2Args &a, double occ_ret, double occ_lim, double agg_ret,
                       double agg_lim) {
     a.filter = p->pb.filter;
@@ -227,6 +264,8 @@ static void fill_args(const are_plan_s *p, K2Args &a, double occ_ret, double occ
     a.stacked = p->tab->d;
     a.rows = p->d_rows;
     a.precombined = p->precombined ? 1 : 0;
+    a.em = p->d_em;
+    a.em_stride = p->em_stride;
 }
 
 }  // namespace are
@@ -501,6 +540,7 @@ int are_plan_free(are_plan_t p) {
     if (!p) return ARE_OK;
     cudaSetDevice(p->device);
     cudaFree(p->d_rows);
+    cudaFree(p->d_em);
     cudaFree(p->d_fin);
     cudaFree(p->d_err);
     cudaFree(p->pb.slots);
@@ -521,6 +561,7 @@ int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ
     if ((rc = choose_variant(p, occ_ret, occ_lim, variant, &v))) return rc;
     DeviceInfo *di;
     if ((rc = use_device(p->device, &di))) return rc;
+    if ((v & 0xFF) == ARE_VARIANT_DENSE && (rc = ensure_event_major(p, di->sms, (cudaStream_t)stream))) return rc;
     K2Args a{};
     a.ids = d_event_ids;
     a.id_base = 0;
@@ -723,6 +764,7 @@ int are_simulate_host(are_plan_t p, const uint32_t *event_ids, int64_t n_occ, co
     ARE_CUDA(cudaEventRecord(w.consumed[0], w.comp));
     ARE_CUDA(cudaEventRecord(w.consumed[1], w.comp));
 
+    if ((v & 0xFF) == ARE_VARIANT_DENSE && (rc = ensure_event_major(p, di->sms, w.comp))) return rc;
     K2Args a{};
     fill_args(p, a, occ_ret, occ_lim, agg_ret, agg_lim);
     a.out = w.d_out;

@@ -318,4 +318,30 @@ int k1_build_plan(const double *d_stacked, int64_t row_len, const int64_t *d_row
     return ARE_OK;
 }
 
+// One thread per (event, selection position), events fastest: the reads of
+// each selected row are coalesced, the writes land in 8-byte slots of
+// consecutive event lines.
+__global__ void k1_event_major_kernel(const double *__restrict__ stacked, int64_t row_len,
+                                      const int64_t *__restrict__ rows, int n_sel, int stride,
+                                      double *__restrict__ em) {
+    const int64_t total = row_len * (int64_t)n_sel;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = i / row_len, e = i - s * row_len;
+        em[e * stride + s] = stacked[rows[s] * row_len + e];
+    }
+}
+
+int k1_event_major(const double *d_stacked, int64_t row_len, const int64_t *d_rows, int n_sel, int stride,
+                   double *d_em, int sms, cudaStream_t st) {
+    ARE_CUDA(cudaMemsetAsync(d_em, 0, (size_t)row_len * stride * sizeof(double), st));
+    const int threads = 256;
+    const int64_t total = row_len * (int64_t)n_sel;
+    int64_t g = (total + threads - 1) / threads;
+    if (g > (int64_t)sms * 16) g = (int64_t)sms * 16;
+    k1_event_major_kernel<<<(unsigned)g, threads, 0, st>>>(d_stacked, row_len, d_rows, n_sel, stride, d_em);
+    ARE_LAUNCHED();
+    return ARE_OK;
+}
+
 }  // namespace are

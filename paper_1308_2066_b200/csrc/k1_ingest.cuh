@@ -22,6 +22,11 @@ int k1_build_plan(const double *d_stacked, int64_t row_len, const int64_t *d_row
 
 int k1_precombine_plan(PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int sms, cudaStream_t st);
 
+// Event-major copy of the selected rows for the dense kernel:
+// em[e * stride + s] = stacked[rows[s] * row_len + e] (s < n_sel; pad = 0).
+int k1_event_major(const double *d_stacked, int64_t row_len, const int64_t *d_rows, int n_sel, int stride,
+                   double *d_em, int sms, cudaStream_t st);
+
 int scan_exclusive_u32(const uint32_t *d_in, uint32_t *d_out, int64_t n, uint64_t *d_tiles,
                        uint64_t *h_total, cudaStream_t st);
 

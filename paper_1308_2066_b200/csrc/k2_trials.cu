@@ -215,7 +215,9 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
 }
 
 // Literal reference loop: every occurrence, every selected row, in order.
-template <int NW>
+// EM: read the occurrence's selected losses from the event-major copy (one
+// 128-byte-aligned line per event when n_sel <= 16) instead of n_sel rows.
+template <int NW, bool EM>
 __global__ void __launch_bounds__(NW * 32) k2_dense(const K2Args a) {
     __shared__ Fin s_fin[ARE_MAX_TABLES];
     __shared__ int64_t s_row[ARE_MAX_TABLES];
@@ -241,6 +243,13 @@ __global__ void __launch_bounds__(NW * 32) k2_dense(const K2Args a) {
                 double comb = 0.0;
                 if (e >= a.row_len) {
                     bad = true;
+                } else if (EM) {
+                    const double2 *line = reinterpret_cast<const double2 *>(a.em + (int64_t)e * a.em_stride);
+                    for (int s = 0; s < a.n_sel; s += 2) {
+                        const double2 v = line[s >> 1];
+                        comb = __dadd_rn(comb, fin_term(s_fin[s], v.x));
+                        if (s + 1 < a.n_sel) comb = __dadd_rn(comb, fin_term(s_fin[s + 1], v.y));
+                    }
                 } else {
                     for (int s = 0; s < a.n_sel; ++s)
                         comb = __dadd_rn(comb, fin_term(s_fin[s], a.stacked[s_row[s] + e]));
@@ -309,7 +318,10 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
     if (variant == ARE_VARIANT_DENSE) {
         int64_t g = (trials + DENSE_WARPS - 1) / DENSE_WARPS;
         const int64_t cap = (int64_t)sms * 8;
-        k2_dense<DENSE_WARPS><<<(unsigned)(g < cap ? g : cap), DENSE_WARPS * 32, 0, st>>>(a);
+        if (a.em)
+            k2_dense<DENSE_WARPS, true><<<(unsigned)(g < cap ? g : cap), DENSE_WARPS * 32, 0, st>>>(a);
+        else
+            k2_dense<DENSE_WARPS, false><<<(unsigned)(g < cap ? g : cap), DENSE_WARPS * 32, 0, st>>>(a);
         ARE_LAUNCHED();
         return ARE_OK;
     }

@@ -33,6 +33,10 @@ struct K2Args {
     const int64_t *rows;
     unsigned int *err;
     int32_t precombined;   // records hold comb (k1_precombine): skip the financial terms
+    // dense variant, event-major copy of the selected rows (k1_event_major):
+    // em[e * em_stride + s] = stacked[rows[s]][e], em_stride even; null = row-major
+    const double *em;
+    int32_t em_stride;
 };
 
 // Threads per CTA of the hot-set kernel (one persistent CTA per SM).

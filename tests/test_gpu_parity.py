@@ -290,10 +290,15 @@ def test_kernel_instantiations_across_hash_modes(catalog):
     want = _oracle_ylt(layer, yet)
     assert np.count_nonzero(want) > 0
     tset = TableSet.from_elts(elts, catalog)
-    for cfg in (HOT, EngineConfig(variant="hotset", precombine=True)):
+    for cfg in (HOT, EngineConfig(variant="hotset", precombine=True), DENSE):
         got, _ = price_layer(yet, tset, None, layer.terms, cfg)
         assert got.tobytes() == want.tobytes()
         assert run_aggregate_analysis([layer], yet, cfg)[0].losses.tobytes() == want.tobytes()
+    # the dense kernel on an odd selection in non-pool order: with >= 64 MB of
+    # selected rows (catalogs 3M, 9M) it reads the event-major copy
+    sub = Layer("S", (elts[3], elts[0], elts[2]), layer.terms)
+    got, _ = price_layer(yet, tset, [3, 0, 2], layer.terms, DENSE)
+    assert got.tobytes() == _oracle_ylt(sub, yet).tobytes()
     second = Layer("M", tuple(elts[1:3]), LayerTerms(0.0, math.inf, 300.0, 20_000.0))
     fused = run_aggregate_analysis([layer, second], yet)
     assert fused[0].losses.tobytes() == want.tobytes()
