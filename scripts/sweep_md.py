@@ -36,8 +36,9 @@ def main() -> None:
                 f"(compulsory-bytes roofline fraction {c['compulsory_frac']:.2f}; algorithmic {c['algorithmic_frac']:.2f})"]
         if "dense" in c:
             dd = c["dense"]
-            out += [f"- dense uncompacted kernel (`k2_dense`, every lookup a float64 gather from the 240 MB tables: "
-                    f"the SURVEY 8(d) \"exceeding L2\" regime): {dd['k2_ms']:.0f} ms -> {dd['trials_per_s'] / 1e6:.1f} M "
+            out += [f"- dense uncompacted kernel (`k2_dense`: every occurrence reads all selected float64 losses, no "
+                    f"hot set; 240 MB of tables, the SURVEY 8(d) \"exceeding L2\" regime, read through an event-major "
+                    f"copy): {dd['k2_ms']:.0f} ms -> {dd['trials_per_s'] / 1e6:.1f} M "
                     f"trials/s (algorithmic fraction {dd['algorithmic_frac']:.2f}), "
                     f"{dd['k2_ms'] / c['k2_ms']:.0f}x slower than the hot-set kernel"]
         out += [""]
