@@ -221,7 +221,7 @@ template <int NW, bool EM>
 __global__ void __launch_bounds__(NW * 32) k2_dense(const K2Args a) {
     __shared__ Fin s_fin[ARE_MAX_TABLES];
     __shared__ int64_t s_row[ARE_MAX_TABLES];
-    __shared__ double s_occ[NW * 32];
+    __shared__ __align__(16) double s_occ[NW * 32];
     for (int i = threadIdx.x; i < a.n_sel; i += blockDim.x) {
         s_fin[i] = a.fin[i];
         s_row[i] = a.rows[i] * (int64_t)a.row_len;
@@ -244,11 +244,20 @@ __global__ void __launch_bounds__(NW * 32) k2_dense(const K2Args a) {
                 if (e >= a.row_len) {
                     bad = true;
                 } else if (EM) {
+                    // the whole line in flight at once (<= 16 tables: one
+                    // 128-byte line), then the terms in selection order
                     const double2 *line = reinterpret_cast<const double2 *>(a.em + (int64_t)e * a.em_stride);
-                    for (int s = 0; s < a.n_sel; s += 2) {
-                        const double2 v = line[s >> 1];
-                        comb = __dadd_rn(comb, fin_term(s_fin[s], v.x));
-                        if (s + 1 < a.n_sel) comb = __dadd_rn(comb, fin_term(s_fin[s + 1], v.y));
+                    for (int s0 = 0; s0 < a.n_sel; s0 += 16) {
+                        double2 v[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            if (s0 + 2 * k < a.n_sel) v[k] = line[(s0 >> 1) + k];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int s = s0 + 2 * k;
+                            if (s < a.n_sel) comb = __dadd_rn(comb, fin_term(s_fin[s], v[k].x));
+                            if (s + 1 < a.n_sel) comb = __dadd_rn(comb, fin_term(s_fin[s + 1], v[k].y));
+                        }
                     }
                 } else {
                     for (int s = 0; s < a.n_sel; ++s)
@@ -258,7 +267,17 @@ __global__ void __launch_bounds__(NW * 32) k2_dense(const K2Args a) {
             }
             __syncwarp();
             const int n = (int)min((int64_t)32, rhi - base);
-            for (int k = 0; k < n; ++k) c = __dadd_rn(c, ob[k]);
+            if (n == 32) {
+                const double2 *ob2 = reinterpret_cast<const double2 *>(ob);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const double2 w = ob2[k];
+                    c = __dadd_rn(c, w.x);
+                    c = __dadd_rn(c, w.y);
+                }
+            } else {
+                for (int k = 0; k < n; ++k) c = __dadd_rn(c, ob[k]);
+            }
             __syncwarp();
         }
         if (lane == 0) a.out[t - a.out_base] = clamp_ref(__dsub_rn(c, a.agg_ret), a.agg_lim);
