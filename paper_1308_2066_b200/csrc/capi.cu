@@ -214,18 +214,20 @@ static int choose_variant(const are_plan_s *p, double occ_ret, double occ_lim, i
     return ARE_OK;
 }
 
-// The dense kernel's event-major table: built once per plan on first use,
-// only when the selected rows exceed what L2 keeps (measured: catalog 2M x 15
-// rows, 240 MB: 7.1 vs 19.1 ms per 100k trials; 200k x 15 rows, 24 MB, stays
-// L2-resident and the row-major walk wins, 5.4 vs 7.1 ms).  If it cannot be
-// allocated the row-major dense kernel runs instead.
-static constexpr int64_t EM_MAX_SEL = 32;
+// The dense kernel's event-major table: built once per plan on first use.
+// Measured, ms per 100k trials x 1000 events (event-major vs row-major):
+// 15 rows over catalogs 2M / 200k / 50k: 4.3 vs 19.1 / 4.3 vs 5.4 / 4.3 vs
+// 5.4; 6 rows over 50k: 2.0 vs 2.5; 3 rows over 50k: 1.7 vs 1.5 -- so the
+// copy is used from 4 selected rows on, or whenever the rows exceed what L2
+// keeps.  If it cannot be allocated the row-major dense kernel runs instead.
+static constexpr int64_t EM_MAX_SEL = 32, EM_MIN_SEL = 4;
 static constexpr int64_t EM_MIN_BYTES = 64ll << 20;
 static int ensure_event_major(are_plan_s *p, int sms, cudaStream_t st) {
     std::lock_guard<std::mutex> g(p->em_mu);
     if (p->em_tried) return ARE_OK;
     p->em_tried = true;
-    if (p->n_sel > EM_MAX_SEL || p->n_sel * p->tab->row_len * (int64_t)sizeof(double) < EM_MIN_BYTES) return ARE_OK;
+    const int64_t bytes_rows = p->n_sel * p->tab->row_len * (int64_t)sizeof(double);
+    if (p->n_sel > EM_MAX_SEL || (p->n_sel < EM_MIN_SEL && bytes_rows < EM_MIN_BYTES)) return ARE_OK;
     const int stride = (int)((p->n_sel + 1) & ~1);
     const size_t bytes = (size_t)p->tab->row_len * stride * sizeof(double);
     double *d = nullptr;
