@@ -211,6 +211,6 @@ class DeviceYearEventTable:
             float(terms.agg_retention), float(terms.agg_limit), out.data_ptr(),
             ctypes.c_void_p(st.cuda_stream),
             _native.VARIANTS[variant] | (_native.IDS_VALIDATED if self.ids_validated else 0)))
-        if check:
+        if check and not self.ids_validated:  # validated ids cannot raise the range flag
             _native.check(lib.are_check_errors(plan.value, ctypes.c_void_p(st.cuda_stream)))
         return out
