@@ -23,5 +23,7 @@ ncu --set full --clock-control none --import-source on -k regex:"^k2_layers_pre$
 timeout 600 python scripts/entry_e2e.py > gpurun_out/entry_e2e_$TAG.json 2> gpurun_out/entry_e2e_$TAG.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_under_ncu_$TAG.log 2>&1
-timeout 1500 python scripts/sweep.py --out gpurun_out/sweep_$TAG.json > gpurun_out/sweep_$TAG.log 2>&1; tail -2 gpurun_out/sweep_$TAG.log
+timeout 1500 python scripts/sweep.py --only c3,c4,c5,refsweeps --out gpurun_out/sweep_$TAG.json > gpurun_out/sweep_$TAG.log 2>&1; tail -2 gpurun_out/sweep_$TAG.log
+python scripts/host_path.py > gpurun_out/host_path_$TAG.log 2>&1
+python scripts/time_density.py > gpurun_out/density_$TAG.log 2>&1
 ls gpurun_out | grep $TAG
