@@ -379,6 +379,9 @@ def test_resident_and_pinned_paths_match_host_path(c1):
     pyet = YearEventTable(yet.catalog_size, pinned, None, yet.offsets)
     got, _ = price_layer(pyet, tset, None, layer.terms)
     assert got.tobytes() == ref.tobytes()
+    # pageable numpy ids (40 MB): staged into the pinned buffers by several threads
+    got, _ = price_layer(yet, tset, None, layer.terms)
+    assert got.tobytes() == ref.tobytes()
 
 
 # ------------------------------------------ full-size properties (C2 shape) --
