@@ -314,7 +314,7 @@ def _layer_table(plan, masks: np.ndarray, lt: np.ndarray, stream) -> _native.Han
 
 
 def simulate_layers_device(dyet, pool_tset: TableSet, masks, terms_list, out=None, variant_flags: int = 0,
-                           precombine: bool = False):
+                           precombine: bool = False, check: bool = True):
     """Fused K2 over a DeviceYearEventTable: (L, T) float64 CUDA tensor of YLTs.
     `precombine` runs the pre-combined variant (SURVEY 8(f) rows 2 + 4): each
     hot event's per-layer occurrence value is evaluated once (K1-L) and K2
@@ -343,7 +343,8 @@ def simulate_layers_device(dyet, pool_tset: TableSet, masks, terms_list, out=Non
                 plan.value, m.shape[0], m.ctypes.data, lt.ctypes.data, dyet.d_ids.data_ptr(), dyet._n_ids,
                 dyet.d_offsets.data_ptr(), n, 0, n, out[g].data_ptr(), n, _native.ctypes.c_void_p(st.cuda_stream),
                 flags))
-    _native.check(lib.are_check_errors(plan.value, _native.ctypes.c_void_p(st.cuda_stream)))
+    if check and not dyet.ids_validated:  # validated ids cannot raise the range flag
+        _native.check(lib.are_check_errors(plan.value, _native.ctypes.c_void_p(st.cuda_stream)))
     return out
 
 
