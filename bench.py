@@ -43,6 +43,7 @@ TRIALS_PER_GPU = 1_000_000
 N_ELTS = 15
 TERMS = (500.0, 10_000.0, 140_000.0, 66_000.0)
 RPS = [10.0, 50.0, 100.0, 250.0]
+E2E_ROUNDS = 3
 SEED = 2066
 METRIC = "aggregate-analysis trials/sec, 1M×1000-event YET, 1/2/4/8 B200; % HBM BW"
 WORKLOAD = "C2: 1M trials x 1000 events/trial per GPU, 1 layer x 15 ELTs, catalog 2M, Cat XL + Agg XL"
@@ -423,14 +424,23 @@ def run_ours(args) -> None:
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    t_e2e = time.perf_counter()
-    e2e_marks = [t_e2e]
-    for _ in range(e2e_steps):
-        e2e_step()
-        e2e_marks.append(time.perf_counter())
-    torch.cuda.synchronize(dev)
-    e2e_s = time.perf_counter() - t_e2e
-    e2e_s = max_over_ranks(e2e_s, dev) if world > 1 else e2e_s
+    # E2E_ROUNDS rounds of e2e_steps steps each; the value is the best round
+    # (every step of it timed, copies included) -- the reference bench's own
+    # convention of the minimum over rounds (pkg/src/aggrisk/bench.py:113-140),
+    # because the box's host is shared and single steps occasionally stall
+    rounds = []
+    for _ in range(E2E_ROUNDS):
+        if world > 1:
+            dist.barrier()
+        t_e2e = time.perf_counter()
+        marks = [t_e2e]
+        for _ in range(e2e_steps):
+            e2e_step()
+            marks.append(time.perf_counter())
+        torch.cuda.synchronize(dev)
+        secs = time.perf_counter() - t_e2e
+        rounds.append((max_over_ranks(secs, dev) if world > 1 else secs, marks))
+    e2e_s, e2e_marks = min(rounds, key=lambda r: r[0])
     e2e_value = total_trials * e2e_steps / e2e_s
     # the PCIe ceiling on this box: one plain pinned->device copy of the ids
     d_probe = torch.empty(pinned.numel(), dtype=torch.int32, device=dev)
@@ -495,8 +505,11 @@ def run_ours(args) -> None:
                 "ms_per_step": e2e_s * 1e3 / e2e_steps, "steps": e2e_steps,
                 "step_ms": [round((b - a) * 1e3, 2) for a, b in zip(e2e_marks, e2e_marks[1:])],
                 "median_step_ms": float(np.median(np.diff(e2e_marks))) * 1e3,
-                "note": "value = all steps over their total time; single steps on a shared host "
-                        "occasionally stall for 0.1-1 s (host memory / PCIe contention), see step_ms",
+                "rounds_ms_per_step": [round(r[0] * 1e3 / e2e_steps, 2) for r in rounds],
+                "note": f"value = the best of {E2E_ROUNDS} rounds of `steps` steps (each round: all its steps "
+                        "over their total time, H2D/D2H included), the reference bench's min-over-rounds "
+                        "convention; single steps on the shared host occasionally stall for 0.1-1 s "
+                        "(rounds_ms_per_step, step_ms of the best round)",
                 "h2d_gbs": h2d / (e2e_s / e2e_steps) / 1e9,
                 "pcie_h2d_gbs_measured": pcie_gbs,
                 "frac_of_pcie": h2d / (e2e_s / e2e_steps) / 1e9 / pcie_gbs,
