@@ -140,12 +140,18 @@ static void parallel_copy(void *dst, const void *src, size_t bytes) {
     const size_t piece = (bytes / n + 63) & ~size_t(63);
     std::vector<std::thread> pool;
     pool.reserve(n - 1);
-    for (size_t i = 1; i < n; ++i) {
-        const size_t a = std::min(bytes, i * piece), b = std::min(bytes, a + piece);
-        if (a < b)
+    size_t done = std::min(bytes, piece);  // [0, done) is this thread's; [launched, bytes) still to copy
+    size_t launched = done;
+    try {
+        for (size_t i = 1; i < n && launched < bytes; ++i) {
+            const size_t a = launched, b = std::min(bytes, a + piece);
             pool.emplace_back([=] { std::memcpy((char *)dst + a, (const char *)src + a, b - a); });
+            launched = b;
+        }
+    } catch (...) {  // no threads available: copy the rest here (never throw across the C ABI)
     }
-    std::memcpy(dst, src, std::min(bytes, piece));
+    std::memcpy(dst, src, done);
+    if (launched < bytes) std::memcpy((char *)dst + launched, (const char *)src + launched, bytes - launched);
     for (auto &t : pool) t.join();
 }
 
