@@ -594,6 +594,7 @@ int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ
     if ((rc = use_device(p->device, &di))) return rc;
     if ((v & 0xFF) == ARE_VARIANT_DENSE && (rc = ensure_event_major(p, di->sms, (cudaStream_t)stream))) return rc;
     K2Args a{};
+    a.mean_len = n_trials > 0 ? (double)n_occ / (double)n_trials : 0.0;
     a.ids = d_event_ids;
     a.id_base = 0;
     a.n_ids = n_occ;
@@ -798,6 +799,7 @@ int are_simulate_host(are_plan_t p, const uint32_t *event_ids, int64_t n_occ, co
     if ((v & 0xFF) == ARE_VARIANT_DENSE && (rc = ensure_event_major(p, di->sms, w.comp))) return rc;
     K2Args a{};
     fill_args(p, a, occ_ret, occ_lim, agg_ret, agg_lim);
+    a.mean_len = (double)(offsets[last] - offsets[first]) / (double)(last - first);
     a.out = w.d_out;
     a.out_base = first;
     a.err = w.d_err;

@@ -214,6 +214,187 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
     if (CHECK && __any_sync(0xffffffffu, emax > last_id) && lane == 0) atomicOr(a.err, 1u);
 }
 
+// ---------------------------------------------------------------------------
+// Paired hot-set kernel (k2_pair): two trials per warp, one per half-warp.
+// Each lane holds its own half's trial (pointers, counters, running sum), so
+// the per-lane state is that of k2_hotset; per step a half filters 4 rows of
+// 16 ids (64 ids of its trial) and appends hits to its own 64-entry queue
+// (one ballot serves both halves).  A batch takes up to 16 queued events per
+// half; lanes past a half's count carry +0.0, so every fold is the unrolled
+// 16-value one (8 LDS.128 + 16 DADD) and advances BOTH trials' chains -- half
+// the fold instructions of k2_hotset -- and the per-trial setup and final
+// flush are shared by the pair.  The float64 sequence per trial is unchanged.
+static constexpr int PH_CAP = 64;  // per-half queue: < 16 pending + 2 rows of 16
+
+template <int HASH, bool CHECK, bool PRE>
+__global__ void __launch_bounds__(K2_THREADS, 1) k2_pair(const K2Args a) {
+    constexpr int NW = K2_THREADS / 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    Fin *s_fin = reinterpret_cast<Fin *>(smem);
+    double *s_occ = reinterpret_cast<double *>(smem + a.fin_bytes);
+    uint32_t *s_q = reinterpret_cast<uint32_t *>(s_occ + NW * 32);
+    uint32_t *s_filter = s_q + NW * QCAP;
+
+    for (int i = threadIdx.x; i < a.n_sel; i += blockDim.x) s_fin[i] = a.fin[i];
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.filter);
+        uint4 *dst = reinterpret_cast<uint4 *>(s_filter);
+        const int n4 = (int)(a.filter_words >> 2);
+        for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int half = lane >> 4, idx = lane & 15;
+    const uint32_t hm = half ? 0xFFFF0000u : 0x0000FFFFu;
+    const uint32_t lth = lanemask_lt() & hm;
+    double *ob = s_occ + warp * 32 + half * 16;  // this half's 16 values
+    const double2 *ob2 = reinterpret_cast<const double2 *>(ob);
+    uint32_t *q = s_q + warp * QCAP + half * PH_CAP;
+    const uint32_t q_saddr = (uint32_t)__cvta_generic_to_shared(q);
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
+    const uint32_t nbits = a.nbits, last_id = a.row_len - 1;
+    const double occ_ret = a.occ_ret, occ_lim = a.occ_lim;
+    const uint32_t *const ids = a.ids;
+    const int64_t WP = (int64_t)gridDim.x * NW;  // pairs in flight
+    uint32_t emax = 0;
+    const uint32_t pad = cold_pad(s_filter, a.filter_words, nbits, a.row_len);
+
+    // this half's next batch entry (record of the idx-th queued event)
+    auto gather = [&](uint32_t qh, uint32_t n) -> Slot {
+        Slot s{0.0, 0u, 0u};
+        if ((uint32_t)idx < n) s = ld_slot(a.slots + q[(qh + idx) & (PH_CAP - 1)], pol_keep);
+        return s;
+    };
+    auto finish = [&](const Slot &s, uint32_t n, double &c) {
+        double v = 0.0;  // lanes past this half's count add +0 (exact: c is never -0)
+        if ((uint32_t)idx < n) {
+            const uint32_t cnt = s.meta >> 16;
+            double comb = 0.0;
+            if (PRE) {
+                if (cnt) comb = s.x;
+            } else {
+                if (cnt) comb = __dadd_rn(0.0, fin_term(s_fin[s.meta & 0xFFFFu], s.x));
+#pragma unroll 1
+                for (uint32_t i = 1; i < cnt; ++i) {
+                    const Entry en = a.ovf[s.ovf + i - 1];
+                    comb = __dadd_rn(comb, fin_term(s_fin[en.j], en.x));
+                }
+            }
+            v = clamp_ref(__dsub_rn(comb, occ_ret), occ_lim);
+        }
+        ob[idx] = v;
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double2 w = ob2[i];
+            c = __dadd_rn(c, w.x);
+            c = __dadd_rn(c, w.y);
+        }
+        __syncwarp();
+    };
+
+    int64_t pr = (int64_t)blockIdx.x * NW + warp;  // pair index
+    const int64_t npairs = (a.last - a.first + 1) / 2;
+    int64_t lo = 0, hi = 0;
+    {
+        const int64_t t = a.first + 2 * pr + half;
+        if (pr < npairs && t < a.last) {
+            lo = a.offsets[t - a.t_base];
+            hi = a.offsets[t - a.t_base + 1];
+        }
+    }
+    for (; pr < npairs; pr += WP) {
+        const int64_t t = a.first + 2 * pr + half;
+        const int64_t tn = t + 2 * WP;
+        int64_t nlo = 0, nhi = 0;
+        if (pr + WP < npairs && tn < a.last) {  // next pair's bounds, in flight
+            nlo = a.offsets[tn - a.t_base];
+            nhi = a.offsets[tn - a.t_base + 1];
+        }
+        const int64_t rlo = lo - a.id_base;
+        const uint32_t len = (uint32_t)(hi - lo);
+        // this half's rows start on a 64-byte boundary; `rel` wraps before
+        // the trial start so one unsigned compare bounds both ends
+        const uint32_t skew = (uint32_t)((reinterpret_cast<uintptr_t>(ids + rlo) >> 2) & 15);
+        const uint32_t *p = ids + (rlo - skew) + idx;
+        uint32_t rel = (uint32_t)idx - skew;
+        const int mych = len ? (int)((len + skew + 63) >> 6) : 0;
+        const int nchunks = __reduce_max_sync(0xffffffffu, (uint32_t)mych);
+        double c = 0.0;
+        uint32_t qh = 0, qt = 0;
+        bool pending = false;
+        Slot ps{0.0, 0u, 0u};
+        uint32_t pn = 0;  // this half's count in the pending batch
+
+        // full batches while both halves hold 16; a half past 32 forces one
+        // (capacity: 2 more rows add <= 32 to a 64-entry queue); need = 1
+        // flushes everything at the end of the pair
+        auto drain = [&](uint32_t need) {
+            while (need == 1u ? __any_sync(0xffffffffu, qt != qh)
+                              : (__all_sync(0xffffffffu, qt - qh >= 16u) || __any_sync(0xffffffffu, qt - qh > 32u))) {
+                const uint32_t n = min(qt - qh, 16u);
+                const Slot ns = gather(qh, n);
+                if (pending) finish(ps, pn, c);
+                ps = ns;
+                pn = n;
+                pending = true;
+                qh += n;
+            }
+        };
+
+        uint32_t r0[4], r1[4], r2[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r0[k] = ld_stream_if(p + 16 * k, rel + 16 * k, len, pol_stream, pad);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r1[k] = ld_stream_if(p + 64 + 16 * k, rel + 64 + 16 * k, len, pol_stream, pad);
+
+        auto step = [&](uint32_t (&cur)[4], uint32_t (&fut)[4]) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 128 + 16 * k, rel + 128 + 16 * k, len, pol_stream, pad);
+            uint32_t ev[4], word[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t e = cur[k];
+                if (CHECK) {
+                    emax = max(emax, e);
+                    e = min(e, last_id);
+                }
+                ev[k] = e;
+                word[k] = s_filter[hot_hash<HASH>(e, nbits) >> 5];
+            }
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+                for (int k = 2 * hf; k < 2 * hf + 2; ++k) {
+                    const bool hot = (word[k] >> (hot_hash<HASH>(ev[k], nbits) & 31)) & 1u;
+                    const uint32_t b = ballot_full(hot);
+                    st_shared_if(q_saddr + (((qt + __popc(b & lth)) & (PH_CAP - 1)) << 2), ev[k], hot);
+                    qt += __popc(b & hm);
+                }
+                __syncwarp();
+                drain(16u);
+            }
+            p += 64;
+            rel += 64;
+        };
+        for (int ch = 0; ch < nchunks; ch += 3) {
+            step(r0, r2);
+            if (ch + 1 >= nchunks) break;
+            step(r1, r0);
+            if (ch + 2 >= nchunks) break;
+            step(r2, r1);
+        }
+        drain(1u);  // whatever either half still holds
+        if (pending) finish(ps, pn, c);
+        if (idx == 0 && t < a.last) a.out[t - a.out_base] = clamp_ref(__dsub_rn(c, a.agg_ret), a.agg_lim);
+        lo = nlo;
+        hi = nhi;
+    }
+    if (CHECK && __any_sync(0xffffffffu, emax > last_id) && lane == 0) atomicOr(a.err, 1u);
+}
+
 // Literal reference loop: every occurrence, every selected row, in order.
 // EM: read the occurrence's selected losses from the event-major copy (one
 // 128-byte-aligned line per event when n_sel <= 16) instead of n_sel rows.
@@ -296,7 +477,21 @@ template <int HASH, bool CHECK, bool PRE>
 static int prepare_one() {
     ARE_CUDA(cudaFuncSetAttribute(k2_hotset<HASH, CHECK, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   k2_max_dynamic_smem()));
+    ARE_CUDA(cudaFuncSetAttribute(k2_pair<HASH, CHECK, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  k2_max_dynamic_smem()));
     return ARE_OK;
+}
+
+// k2_pair wins on short trials (measured, ms per 1e9 ids, pair vs hotset:
+// E=100 3.57 vs 4.37, E=250 3.04 vs 3.19) and loses on long ones (E=500 2.89
+// vs 2.73, E=1000 2.92 vs 2.52).  ARE_K2_PAIR=0/1 forces a kernel (A/B).
+static constexpr double PAIR_MAX_MEAN_LEN = 320.0;
+static bool use_pair(double mean_len) {
+    static const int force = [] {
+        const char *e = getenv("ARE_K2_PAIR");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    return force >= 0 ? force == 1 : mean_len <= PAIR_MAX_MEAN_LEN;
 }
 
 template <bool PRE>
@@ -319,6 +514,17 @@ int k2_prepare(int device) {
 
 template <bool PRE>
 static void launch_hotset(const K2Args &a, int sel, dim3 grid, dim3 block, size_t smem, cudaStream_t st) {
+    if (use_pair(a.mean_len)) {
+        switch (sel) {
+            case 0: k2_pair<0, false, PRE><<<grid, block, smem, st>>>(a); break;
+            case 1: k2_pair<0, true, PRE><<<grid, block, smem, st>>>(a); break;
+            case 2: k2_pair<1, false, PRE><<<grid, block, smem, st>>>(a); break;
+            case 3: k2_pair<1, true, PRE><<<grid, block, smem, st>>>(a); break;
+            case 4: k2_pair<2, false, PRE><<<grid, block, smem, st>>>(a); break;
+            default: k2_pair<2, true, PRE><<<grid, block, smem, st>>>(a); break;
+        }
+        return;
+    }
     switch (sel) {
         case 0: k2_hotset<0, false, PRE><<<grid, block, smem, st>>>(a); break;
         case 1: k2_hotset<0, true, PRE><<<grid, block, smem, st>>>(a); break;

@@ -37,6 +37,9 @@ struct K2Args {
     // em[e * em_stride + s] = stacked[rows[s]][e], em_stride even; null = row-major
     const double *em;
     int32_t em_stride;
+    // mean occurrences per trial of the launch (host estimate): short trials
+    // run the paired kernel (k2_pair), long ones k2_hotset
+    double mean_len;
 };
 
 // Threads per CTA of the hot-set kernel (one persistent CTA per SM).

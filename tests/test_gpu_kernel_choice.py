@@ -1,0 +1,31 @@
+"""Both hot-set kernels over the parity suite.
+
+The library runs k2_pair (two trials per warp) for launches whose mean trial
+is short and k2_hotset otherwise (csrc/k2_trials.cu `use_pair`), so in a
+normal run each parity test exercises one of them.  ARE_K2_PAIR=0/1 forces
+one kernel for the whole process; this runs the core parity tests under each
+in a subprocess so both kernels meet every case.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CASES = ("random_instances or plugin_run_trials or worked or empty_trial or c1_ylt or seed31 or nan_inf "
+         "or large_catalogs or 256_tables or long_and_ragged or instantiations or resident_and_pinned")
+
+
+@pytest.mark.parametrize("force", ["0", "1"], ids=["k2_hotset", "k2_pair"])
+def test_parity_suite_under_each_kernel(force):
+    env = dict(os.environ, ARE_K2_PAIR=force)
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-q",
+                        "-x", "-p", "no:cacheprovider", "-k", CASES], cwd=ROOT, env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
