@@ -261,10 +261,14 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_pair(const K2Args a) {
     uint32_t emax = 0;
     const uint32_t pad = cold_pad(s_filter, a.filter_words, nbits, a.row_len);
 
-    // this half's next batch entry (record of the idx-th queued event)
+    // this half's next batch entry (record of the idx-th queued event); the
+    // ring slot just read may be rewritten by another lane's later append
     auto gather = [&](uint32_t qh, uint32_t n) -> Slot {
+        uint32_t ev = 0;
+        if ((uint32_t)idx < n) ev = q[(qh + idx) & (PH_CAP - 1)];
+        __syncwarp();
         Slot s{0.0, 0u, 0u};
-        if ((uint32_t)idx < n) s = ld_slot(a.slots + q[(qh + idx) & (PH_CAP - 1)], pol_keep);
+        if ((uint32_t)idx < n) s = ld_slot(a.slots + ev, pol_keep);
         return s;
     };
     auto finish = [&](const Slot &s, uint32_t n, double &c) {
