@@ -9,7 +9,8 @@ with random occurrence / aggregate terms; then compares, bit for bit:
   * the same with EngineConfig(precombine=True),
   * price_layer per layer with the dense kernel,
   * a DeviceYearEventTable run,
-against oracle.run_trials_port per layer.
+against oracle.run_trials_port per layer; and K3 (PML exact, TVaR rel 1e-12)
+plus the portfolio roll-up on every YLT.
 
     python scripts/fuzz_parity.py [--seconds 300] [--seed 1]
 """
@@ -32,6 +33,7 @@ from paper_1308_2066_b200.errors import PortfolioInvalidError  # noqa: E402
 from paper_1308_2066_b200.portfolio import (EventLossTable, FinancialTerms, Layer, LayerTerms,  # noqa: E402
                                             YearEventTable)
 from paper_1308_2066_b200.resident import DeviceYearEventTable  # noqa: E402
+from paper_1308_2066_b200.risk import order_stats, portfolio_rollup  # noqa: E402
 
 
 def want_ylt(layer, yet):
@@ -91,6 +93,23 @@ def main() -> None:
             got = run_aggregate_analysis(layers, yet, cfg)
             for lay, w, g in zip(layers, wants, got):
                 assert g.losses.tobytes() == w.tobytes(), (n, lay.id, cfg)
+        # K3 on every YLT and on the portfolio roll-up: PML exact, TVaR rel 1e-12
+        ylts = list(got)
+        roll = portfolio_rollup(ylts).losses
+        want_roll = np.zeros(yet.trial_count)
+        for w in wants:
+            want_roll = want_roll + w  # list order, like metrics.py:118-133
+        assert roll.tobytes() == want_roll.tobytes(), (n, "rollup")
+        n_tr = yet.trial_count
+        rps = [rp for rp in (1.5, 2.0, 10.0, 50.0, 100.0, 250.0, float(n_tr)) if 1.0 < rp <= n_tr]
+        for w in wants + [want_roll]:
+            if not rps:
+                break
+            p, t = order_stats(w, rps)
+            for rp, pv, tv in zip(rps, p, t):
+                assert pv == oracle.pml(w, rp), (n, "pml", rp)
+                ref = oracle.tvar(w, rp)
+                assert abs(tv - ref) <= 1e-12 * max(abs(ref), 1e-300) or (math.isnan(tv) and math.isnan(ref)), (n, "tvar")
         dyet = DeviceYearEventTable(yet)
         got = run_aggregate_analysis(layers, dyet)
         for w, g in zip(wants, got):
