@@ -323,11 +323,14 @@ def run_ours(args) -> None:
         raise SystemExit("bench.py: no CUDA device -- the B200 engine has no CPU fallback")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # ARE_BENCH_BACKEND=gloo lets several ranks share one GPU, to exercise the
+    # multi-rank control flow on a one-GPU box (NCCL refuses duplicate GPUs)
+    backend = os.environ.get("ARE_BENCH_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     threads = max(1, host_cores() // max(world, 1))
 
     layer = make_layer()
@@ -484,7 +487,7 @@ def run_ours(args) -> None:
         "config": {
             "workload": WORKLOAD, "trials_per_gpu": TRIALS_PER_GPU, "events_per_trial": EVENTS,
             "elts": N_ELTS, "catalog": CATALOG, "layer_terms": list(TERMS), "return_periods": RPS,
-            "parallelism": f"trial-sharded x{world} (split_by_events), YLT all-gather over NCCL",
+            "parallelism": f"trial-sharded x{world} (split_by_events), YLT all-gather over {backend.upper()}",
             "l2": "no flush: 4 GB id stream per GPU > 126 MB L2; hot-set records L2-resident by design",
             "generator": "ELTs: reference generator restatement seed 2066; YET: synth.bulk_yet",
             "kernel": "k2_hotset (persistent, 1 CTA/SM, warp per trial)",
