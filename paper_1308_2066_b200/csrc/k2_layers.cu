@@ -196,8 +196,17 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
             layer_eval(s, a.ovf, s_fin, s_mask, s_occ_ret, s_occ_lim, nl, sg, occ + si * K2L_MAX_LAYERS);
         }
         __syncwarp();
-        if (lane < nl)
-            for (uint32_t i = 0; i < n; ++i) c = __dadd_rn(c, occ[i * K2L_MAX_LAYERS + lane]);
+        if (lane < nl) {
+            if (n == (uint32_t)LSUB) {  // full sub-batch: all loads first, then the in-order chain
+                double v[LSUB];
+#pragma unroll
+                for (int i = 0; i < LSUB; ++i) v[i] = occ[i * K2L_MAX_LAYERS + lane];
+#pragma unroll
+                for (int i = 0; i < LSUB; ++i) c = __dadd_rn(c, v[i]);
+            } else {
+                for (uint32_t i = 0; i < n; ++i) c = __dadd_rn(c, occ[i * K2L_MAX_LAYERS + lane]);
+            }
+        }
         __syncwarp();
     };
 
