@@ -402,8 +402,11 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_pair(const K2Args a) {
 // Literal reference loop: every occurrence, every selected row, in order.
 // EM: read the occurrence's selected losses from the event-major copy (one
 // 128-byte-aligned line per event when n_sel <= 16) instead of n_sel rows.
+// At most 64 registers (4 CTAs of 256 threads per SM), one resident wave;
+// the next row's ids load while the current row's lines are in flight.
+static constexpr int DENSE_CTAS_PER_SM = 4;
 template <int NW, bool EM>
-__global__ void __launch_bounds__(NW * 32) k2_dense(const K2Args a) {
+__global__ void __launch_bounds__(NW * 32, DENSE_CTAS_PER_SM) k2_dense(const K2Args a) {
     __shared__ Fin s_fin[ARE_MAX_TABLES];
     __shared__ int64_t s_row[ARE_MAX_TABLES];
     __shared__ __align__(16) double s_occ[NW * 32];
@@ -421,10 +424,12 @@ __global__ void __launch_bounds__(NW * 32) k2_dense(const K2Args a) {
         const int64_t rlo = a.offsets[t - a.t_base] - a.id_base;
         const int64_t rhi = a.offsets[t - a.t_base + 1] - a.id_base;
         double c = 0.0;
+        uint32_t e_next = rlo + lane < rhi ? ld_stream_u32(a.ids + rlo + lane, pol_stream) : 0u;
         for (int64_t base = rlo; base < rhi; base += 32) {
             const int64_t i = base + lane;
+            const uint32_t e = e_next;
+            if (i + 32 < rhi) e_next = ld_stream_u32(a.ids + i + 32, pol_stream);
             if (i < rhi) {
-                const uint32_t e = ld_stream_u32(a.ids + i, pol_stream);
                 double comb = 0.0;
                 if (e >= a.row_len) {
                     bad = true;
@@ -470,7 +475,109 @@ __global__ void __launch_bounds__(NW * 32) k2_dense(const K2Args a) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.err, 1u);
 }
 
+// Dense kernel over the event-major copy with cooperative line loads: eight
+// lanes read one event's 128-byte line (one 16-byte load each), so one warp
+// load brings four events' lines, where k2_dense<EM> has every lane load its
+// own event's line in eight 16-byte pieces (random 128-byte lines from a
+// 256 MB table, scripts/micro/rand_lines.cu: 9.2 vs 4.6 TB/s).  Each lane
+// applies the financial terms of its two slots of the line; the values pass
+// through shared memory so that the event's own lane adds them in selection
+// order -- the reference's comb sequence, bit for bit.  Rows of FS = stride
+// + 2 doubles keep the per-event 16-byte reads conflict-free.
+static constexpr int COOP_CTAS_PER_SM = 3;  // 85 registers: the eight lines per lane in flight without spills
+template <int NW, int PASSES>
+__global__ void __launch_bounds__(NW * 32, COOP_CTAS_PER_SM) k2_dense_coop(const K2Args a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int S2 = a.em_stride >> 1;  // 16-byte pieces per event, <= 8 * PASSES
+    const int FS = a.em_stride + 2;
+    Fin *s_fin = reinterpret_cast<Fin *>(smem);
+    double *s_occ = reinterpret_cast<double *>(s_fin + 16 * PASSES);
+    double *s_f = s_occ + NW * 32;
+    for (int i = threadIdx.x; i < 16 * PASSES; i += blockDim.x) s_fin[i] = i < a.n_sel ? a.fin[i] : Fin{0.0, 0.0, 0.0, 0.0};
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k = lane & 7, sub = lane >> 3;  // piece of the line, event within a group of four
+    double *ob = s_occ + warp * 32;
+    double *fw = s_f + (size_t)warp * 32 * FS;  // fw[event of the row * FS + slot]
+    const double2 *em2 = reinterpret_cast<const double2 *>(a.em);
+    const uint64_t pol_stream = policy_evict_first();
+    const Fin fa = s_fin[2 * k], fb = s_fin[2 * k + 1];  // this lane's slots in pass 0
+    const int n_sel = a.n_sel;
+    bool bad = false;
+    for (int64_t t = a.first + (int64_t)blockIdx.x * NW + warp; t < a.last;
+         t += (int64_t)gridDim.x * NW) {
+        const int64_t rlo = a.offsets[t - a.t_base] - a.id_base;
+        const int64_t rhi = a.offsets[t - a.t_base + 1] - a.id_base;
+        double c = 0.0;
+        uint32_t e_next = rlo + lane < rhi ? ld_stream_u32(a.ids + rlo + lane, pol_stream) : 0u;
+        for (int64_t base = rlo; base < rhi; base += 32) {
+            const int64_t i = base + lane;
+            uint32_t e = e_next;
+            if (i + 32 < rhi) e_next = ld_stream_u32(a.ids + i + 32, pol_stream);
+            const bool own = i < rhi;
+            const bool ebad = own && e >= a.row_len;
+            bad |= ebad;
+            if (!own || ebad) e = 0;  // row 0 of the copy: a valid address, result unused
+#pragma unroll
+            for (int p = 0; p < PASSES; ++p) {
+                const int kk = k + 8 * p;
+                double2 v[8];
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    const uint32_t eg = __shfl_sync(0xffffffffu, e, 4 * g + sub);
+                    v[g] = make_double2(0.0, 0.0);
+                    if (kk < S2) v[g] = __ldg(em2 + (size_t)eg * S2 + kk);
+                }
+                const Fin &f0 = p == 0 ? fa : s_fin[2 * kk];
+                const Fin &f1 = p == 0 ? fb : s_fin[2 * kk + 1];
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    if (kk < S2) {
+                        const double2 f = make_double2(fin_term(f0, v[g].x), fin_term(f1, v[g].y));
+                        *reinterpret_cast<double2 *>(fw + (4 * g + sub) * FS + 2 * kk) = f;
+                    }
+                }
+            }
+            __syncwarp();
+            if (own) {
+                const double *row = fw + lane * FS;
+                double comb = 0.0;
+                int s = 0;
+                for (; s + 1 < n_sel; s += 2) {
+                    const double2 w = *reinterpret_cast<const double2 *>(row + s);
+                    comb = __dadd_rn(comb, w.x);
+                    comb = __dadd_rn(comb, w.y);
+                }
+                if (s < n_sel) comb = __dadd_rn(comb, row[s]);
+                if (ebad) comb = 0.0;
+                ob[lane] = clamp_ref(__dsub_rn(comb, a.occ_ret), a.occ_lim);
+            }
+            __syncwarp();
+            const int n = (int)min((int64_t)32, rhi - base);
+            if (n == 32) {
+                const double2 *ob2 = reinterpret_cast<const double2 *>(ob);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const double2 w = ob2[q];
+                    c = __dadd_rn(c, w.x);
+                    c = __dadd_rn(c, w.y);
+                }
+            } else {
+                for (int q = 0; q < n; ++q) c = __dadd_rn(c, ob[q]);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) a.out[t - a.out_base] = clamp_ref(__dsub_rn(c, a.agg_ret), a.agg_lim);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.err, 1u);
+}
+
 static constexpr int DENSE_WARPS = 8;
+static size_t dense_coop_smem(int em_stride) {
+    const int passes = em_stride > 16 ? 2 : 1;
+    return (size_t)16 * passes * sizeof(Fin) + (size_t)DENSE_WARPS * 32 * sizeof(double) +
+           (size_t)DENSE_WARPS * 32 * (em_stride + 2) * sizeof(double);
+}
 
 size_t k2_hotset_fixed_smem(int n_sel) {
     constexpr int NW = K2_THREADS / 32;
@@ -498,6 +605,15 @@ static bool use_pair(double mean_len) {
     return force >= 0 ? force == 1 : mean_len <= PAIR_MAX_MEAN_LEN;
 }
 
+// ARE_DENSE_COOP=0 runs the lane-per-event event-major kernel instead (A/B).
+static bool dense_coop_off() {
+    static const bool off = [] {
+        const char *e = getenv("ARE_DENSE_COOP");
+        return e && e[0] == '0';
+    }();
+    return off;
+}
+
 template <bool PRE>
 static int prepare_pre() {
     int rc;
@@ -512,6 +628,10 @@ int k2_prepare(int device) {
     (void)device;
     int rc;
     if ((rc = prepare_pre<false>()) || (rc = prepare_pre<true>())) return rc;
+    ARE_CUDA(cudaFuncSetAttribute(k2_dense_coop<DENSE_WARPS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)dense_coop_smem(16)));
+    ARE_CUDA(cudaFuncSetAttribute(k2_dense_coop<DENSE_WARPS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)dense_coop_smem(32)));
     if ((rc = k2_layers_prepare())) return rc;
     return k2_layers_pre_prepare();
 }
@@ -546,8 +666,16 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
     variant &= 0xFF;
     if (variant == ARE_VARIANT_DENSE) {
         int64_t g = (trials + DENSE_WARPS - 1) / DENSE_WARPS;
-        const int64_t cap = (int64_t)sms * 8;
-        if (a.em)
+        const int64_t cap = (int64_t)sms * DENSE_CTAS_PER_SM;
+        const int64_t ccap = (int64_t)sms * COOP_CTAS_PER_SM;
+        if (a.em && !dense_coop_off())
+            if (a.em_stride <= 16)
+                k2_dense_coop<DENSE_WARPS, 1><<<(unsigned)(g < ccap ? g : ccap), DENSE_WARPS * 32,
+                                                dense_coop_smem(a.em_stride), st>>>(a);
+            else
+                k2_dense_coop<DENSE_WARPS, 2><<<(unsigned)(g < ccap ? g : ccap), DENSE_WARPS * 32,
+                                                dense_coop_smem(a.em_stride), st>>>(a);
+        else if (a.em)
             k2_dense<DENSE_WARPS, true><<<(unsigned)(g < cap ? g : cap), DENSE_WARPS * 32, 0, st>>>(a);
         else
             k2_dense<DENSE_WARPS, false><<<(unsigned)(g < cap ? g : cap), DENSE_WARPS * 32, 0, st>>>(a);

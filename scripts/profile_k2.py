@@ -1,6 +1,9 @@
 """Minimal driver for ncu: C2 setup (bench.py's data), then a few K2 launches.
 
-    python scripts/profile_k2.py [--variant hotset|dense] [--launches N] [--trials T]
+    python scripts/profile_k2.py [--variant hotset|dense] [--launches N] [--trials T] [--events E]
+
+--events changes the occurrences per trial (C5's short-trial points run
+k2_pair below 320 occurrences per trial).
 """
 
 from __future__ import annotations
@@ -27,10 +30,12 @@ def main() -> None:
     ap.add_argument("--variant", default="hotset")
     ap.add_argument("--launches", type=int, default=3)
     ap.add_argument("--trials", type=int, default=bench.TRIALS_PER_GPU)
+    ap.add_argument("--events", type=int, default=bench.EVENTS)
     ap.add_argument("--k3", action="store_true")
     ap.add_argument("--h2d", action="store_true", help="also time a pinned 4 GB H2D copy")
     args = ap.parse_args()
     layer = bench.make_layer()
+    bench.EVENTS = args.events
     yet = bench.make_yet(0, args.trials, os.cpu_count() or 8)
     tset = TableSet.from_elts(layer.elts, bench.CATALOG)
     plan = tset.plan(*tset.selection_arrays(None))

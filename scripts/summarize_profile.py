@@ -30,6 +30,7 @@ def main() -> None:
     ap.add_argument("out")
     ap.add_argument("--traffic-json")
     ap.add_argument("--launches")
+    ap.add_argument("--workload", default="C2 workload")
     args = ap.parse_args()
 
     raw = ncu(args.rep, "--page", "raw")
@@ -45,7 +46,7 @@ def main() -> None:
     dur = val("gpu__time_duration.sum")
     rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
     lines = [f"# ncu summary: {m['Kernel Name'][0] if 'Kernel Name' in m else 'kernel'}", "",
-             f"source report: `{args.rep}` (ncu --set full --clock-control none, 1 launch, C2 workload)", "",
+             f"source report: `{args.rep}` (ncu --set full --clock-control none, 1 launch, {args.workload})", "",
              "| metric | value |", "|---|---|"]
     rows = [
         ("duration (ms, serialised, cold-ish)", f"{dur * 1e3:.3f}"),
