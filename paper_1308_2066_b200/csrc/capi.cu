@@ -228,12 +228,28 @@ static bool occ_zero_ok(double occ_ret, double occ_lim) {
     return o == 0.0;
 }
 
+// AUTO also picks the dense kernel for dense-overlap plans, where the hot set
+// gathers several scattered entries per occurrence and the cooperative
+// event-major kernel reads one line instead.  Measured, ms per 100k trials x
+// 1000 events, hot set vs dense (scripts/time_density.py): catalog 50k with
+// 15 ELTs (6 entries per catalog event) 4.08 vs 2.06; 6 ELTs (2.4) 1.80 vs
+// 2.00; 3 ELTs 1.03 vs 1.27; catalog 200k, 15 ELTs (1.5) 1.33 vs 2.06;
+// catalog 2M, 15 ELTs (0.15) 0.28 vs 2.47.  Pre-combined plans read one value
+// per event on the hot set and always keep it.
+static constexpr double DENSE_MIN_ENTRIES_PER_EVENT = 3.5;
+static constexpr int64_t EM_MAX_SEL = 32, EM_MIN_SEL = 4;  // the event-major copy (ensure_event_major)
+static constexpr int64_t EM_MIN_BYTES = 64ll << 20;
+static bool dense_overlap(const are_plan_s *p) {
+    return !p->precombined && p->n_sel >= EM_MIN_SEL && p->n_sel <= EM_MAX_SEL &&
+           (double)p->pb.entries >= DENSE_MIN_ENTRIES_PER_EVENT * (double)p->tab->row_len;
+}
+
 static int choose_variant(const are_plan_s *p, double occ_ret, double occ_lim, int variant, int *out) {
     const int flags = variant & ~0xFF;
     variant &= 0xFF;
     const bool exact = p->zero_skip && !p->slot0_hot && occ_zero_ok(occ_ret, occ_lim);
     if (variant == ARE_VARIANT_AUTO) {
-        *out = (exact ? ARE_VARIANT_HOTSET : ARE_VARIANT_DENSE) | flags;
+        *out = (exact && !dense_overlap(p) ? ARE_VARIANT_HOTSET : ARE_VARIANT_DENSE) | flags;
         return ARE_OK;
     }
     if (variant == ARE_VARIANT_HOTSET && !exact)
@@ -249,8 +265,6 @@ static int choose_variant(const are_plan_s *p, double occ_ret, double occ_lim, i
 // 5.4; 6 rows over 50k: 2.0 vs 2.5; 3 rows over 50k: 1.7 vs 1.5 -- so the
 // copy is used from 4 selected rows on, or whenever the rows exceed what L2
 // keeps.  If it cannot be allocated the row-major dense kernel runs instead.
-static constexpr int64_t EM_MAX_SEL = 32, EM_MIN_SEL = 4;
-static constexpr int64_t EM_MIN_BYTES = 64ll << 20;
 static int ensure_event_major(are_plan_s *p, int sms, cudaStream_t st) {
     std::lock_guard<std::mutex> g(p->em_mu);
     if (p->em_tried) return ARE_OK;

@@ -47,8 +47,9 @@ class EngineConfig:
     `worker_count` and `chunk_size` keep their reference validation; the
     GPU result does not depend on them (the reference guarantees bit-identity
     across both, test_engine.py:93-103, and so does this engine).
-    `variant` selects the K2 kernel: "auto" (hot-set when exact, else
-    dense), "hotset" or "dense".
+    `variant` selects the K2 kernel: "auto" (hot-set when exact, unless the
+    plan is dense-overlap -- >= 3.5 table entries per catalog event, where the
+    event-major dense kernel is faster -- else dense), "hotset" or "dense".
     """
 
     worker_count: int = 1

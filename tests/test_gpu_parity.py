@@ -336,6 +336,34 @@ def test_long_and_ragged_trials():
         assert got.tobytes() == _oracle_ylt(layer, sub).tobytes()
 
 
+@pytest.mark.parametrize("n_sel", [4, 5, 15, 16, 17, 31, 32])
+def test_dense_overlap_plans_event_major_kernel(n_sel):
+    """Dense-overlap plans (several entries per catalog event: the reference's
+    own bench shape) run the cooperative event-major dense kernel under AUTO;
+    one and two line passes, odd selections (a padded slot), ragged trials and
+    non-identity financial terms, all bitwise equal to the reference loop."""
+    cat = 1_000
+    rng = np.random.default_rng(n_sel)
+    elts = tuple(EventLossTable(cat, np.sort(rng.choice(np.arange(1, cat + 1), 400, replace=False)).astype(np.uint32),
+                                rng.lognormal(0, 1, 400) * 100,
+                                FinancialTerms(float(rng.uniform(0.5, 1.5)), float(rng.uniform(0, 20)),
+                                               float(rng.choice([math.inf, 150.0])), float(rng.uniform(0.2, 1.0))))
+                 for _ in range(n_sel))
+    layer = Layer("dense", elts, LayerTerms(30.0, 2_000.0, 100.0, 50_000.0))
+    lens = rng.integers(0, 300, 200)
+    lens[:6] = [0, 1, 31, 32, 33, 64]
+    yet = YearEventTable(cat, rng.integers(1, cat + 1, int(lens.sum())).astype(np.uint32), None,
+                         np.concatenate([[0], np.cumsum(lens)]).astype(np.int64))
+    want = _oracle_ylt(layer, yet).tobytes()
+    tset = TableSet.from_elts(layer.elts, cat)
+    for cfg in (EngineConfig(), HOT, DENSE):
+        got, _ = price_layer(yet, tset, None, layer.terms, cfg)
+        assert got.tobytes() == want, cfg
+    bad = YearEventTable(cat, np.array([4, cat + 1, 9], np.uint32), None, np.array([0, 3], np.int64))
+    with pytest.raises(EventOutOfRangeError):
+        price_layer(bad, tset, None, layer.terms, DENSE)
+
+
 def test_loss_in_unused_slot_zero_is_honoured():
     """A dense table with a loss in column 0 (the reference reads it for event
     id 0) routes to the dense kernel and still matches the reference loop."""
