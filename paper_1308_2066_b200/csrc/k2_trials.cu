@@ -485,11 +485,13 @@ __global__ void __launch_bounds__(NW * 32, DENSE_CTAS_PER_SM) k2_dense(const K2A
 // order -- the reference's comb sequence, bit for bit.  Rows of FS = stride
 // + 2 doubles keep the per-event 16-byte reads conflict-free.
 static constexpr int COOP_CTAS_PER_SM = 3;  // 85 registers: the eight lines per lane in flight without spills
-template <int NW, int PASSES>
+// FULL: the stride is exactly 16 * PASSES (15-16 or 31-32 selected rows), so
+// the line shape is a compile-time constant.
+template <int NW, int PASSES, bool FULL>
 __global__ void __launch_bounds__(NW * 32, COOP_CTAS_PER_SM) k2_dense_coop(const K2Args a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int S2 = a.em_stride >> 1;  // 16-byte pieces per event, <= 8 * PASSES
-    const int FS = a.em_stride + 2;
+    const int S2 = FULL ? 8 * PASSES : a.em_stride >> 1;  // 16-byte pieces per event
+    const int FS = 2 * S2 + 2;
     Fin *s_fin = reinterpret_cast<Fin *>(smem);
     double *s_occ = reinterpret_cast<double *>(s_fin + 16 * PASSES);
     double *s_f = s_occ + NW * 32;
@@ -525,14 +527,18 @@ __global__ void __launch_bounds__(NW * 32, COOP_CTAS_PER_SM) k2_dense_coop(const
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
                     const uint32_t eg = __shfl_sync(0xffffffffu, e, 4 * g + sub);
-                    v[g] = make_double2(0.0, 0.0);
-                    if (kk < S2) v[g] = __ldg(em2 + (size_t)eg * S2 + kk);
+                    if (FULL) {
+                        v[g] = __ldg(em2 + (size_t)eg * S2 + kk);
+                    } else {
+                        v[g] = make_double2(0.0, 0.0);
+                        if (kk < S2) v[g] = __ldg(em2 + (size_t)eg * S2 + kk);
+                    }
                 }
                 const Fin &f0 = p == 0 ? fa : s_fin[2 * kk];
                 const Fin &f1 = p == 0 ? fb : s_fin[2 * kk + 1];
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
-                    if (kk < S2) {
+                    if (FULL || kk < S2) {
                         const double2 f = make_double2(fin_term(f0, v[g].x), fin_term(f1, v[g].y));
                         *reinterpret_cast<double2 *>(fw + (4 * g + sub) * FS + 2 * kk) = f;
                     }
@@ -542,13 +548,26 @@ __global__ void __launch_bounds__(NW * 32, COOP_CTAS_PER_SM) k2_dense_coop(const
             if (own) {
                 const double *row = fw + lane * FS;
                 double comb = 0.0;
-                int s = 0;
-                for (; s + 1 < n_sel; s += 2) {
-                    const double2 w = *reinterpret_cast<const double2 *>(row + s);
+                if (FULL) {  // n_sel is 2 * S2 - 1 or 2 * S2
+                    const double2 *row2 = reinterpret_cast<const double2 *>(row);
+#pragma unroll
+                    for (int q = 0; q < S2 - 1; ++q) {
+                        const double2 w = row2[q];
+                        comb = __dadd_rn(comb, w.x);
+                        comb = __dadd_rn(comb, w.y);
+                    }
+                    const double2 w = row2[S2 - 1];
                     comb = __dadd_rn(comb, w.x);
-                    comb = __dadd_rn(comb, w.y);
+                    if (n_sel == 2 * S2) comb = __dadd_rn(comb, w.y);
+                } else {
+                    int s = 0;
+                    for (; s + 1 < n_sel; s += 2) {
+                        const double2 w = *reinterpret_cast<const double2 *>(row + s);
+                        comb = __dadd_rn(comb, w.x);
+                        comb = __dadd_rn(comb, w.y);
+                    }
+                    if (s < n_sel) comb = __dadd_rn(comb, row[s]);
                 }
-                if (s < n_sel) comb = __dadd_rn(comb, row[s]);
                 if (ebad) comb = 0.0;
                 ob[lane] = clamp_ref(__dsub_rn(comb, a.occ_ret), a.occ_lim);
             }
@@ -628,9 +647,13 @@ int k2_prepare(int device) {
     (void)device;
     int rc;
     if ((rc = prepare_pre<false>()) || (rc = prepare_pre<true>())) return rc;
-    ARE_CUDA(cudaFuncSetAttribute(k2_dense_coop<DENSE_WARPS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ARE_CUDA(cudaFuncSetAttribute(k2_dense_coop<DENSE_WARPS, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)dense_coop_smem(16)));
-    ARE_CUDA(cudaFuncSetAttribute(k2_dense_coop<DENSE_WARPS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ARE_CUDA(cudaFuncSetAttribute(k2_dense_coop<DENSE_WARPS, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)dense_coop_smem(16)));
+    ARE_CUDA(cudaFuncSetAttribute(k2_dense_coop<DENSE_WARPS, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)dense_coop_smem(32)));
+    ARE_CUDA(cudaFuncSetAttribute(k2_dense_coop<DENSE_WARPS, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)dense_coop_smem(32)));
     if ((rc = k2_layers_prepare())) return rc;
     return k2_layers_pre_prepare();
@@ -668,14 +691,18 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
         int64_t g = (trials + DENSE_WARPS - 1) / DENSE_WARPS;
         const int64_t cap = (int64_t)sms * DENSE_CTAS_PER_SM;
         const int64_t ccap = (int64_t)sms * COOP_CTAS_PER_SM;
-        if (a.em && !dense_coop_off())
-            if (a.em_stride <= 16)
-                k2_dense_coop<DENSE_WARPS, 1><<<(unsigned)(g < ccap ? g : ccap), DENSE_WARPS * 32,
-                                                dense_coop_smem(a.em_stride), st>>>(a);
+        const unsigned cg = (unsigned)(g < ccap ? g : ccap);
+        const size_t csm = dense_coop_smem(a.em_stride);
+        if (a.em && !dense_coop_off()) {
+            if (a.em_stride == 16)
+                k2_dense_coop<DENSE_WARPS, 1, true><<<cg, DENSE_WARPS * 32, csm, st>>>(a);
+            else if (a.em_stride < 16)
+                k2_dense_coop<DENSE_WARPS, 1, false><<<cg, DENSE_WARPS * 32, csm, st>>>(a);
+            else if (a.em_stride == 32)
+                k2_dense_coop<DENSE_WARPS, 2, true><<<cg, DENSE_WARPS * 32, csm, st>>>(a);
             else
-                k2_dense_coop<DENSE_WARPS, 2><<<(unsigned)(g < ccap ? g : ccap), DENSE_WARPS * 32,
-                                                dense_coop_smem(a.em_stride), st>>>(a);
-        else if (a.em)
+                k2_dense_coop<DENSE_WARPS, 2, false><<<cg, DENSE_WARPS * 32, csm, st>>>(a);
+        } else if (a.em)
             k2_dense<DENSE_WARPS, true><<<(unsigned)(g < cap ? g : cap), DENSE_WARPS * 32, 0, st>>>(a);
         else
             k2_dense<DENSE_WARPS, false><<<(unsigned)(g < cap ? g : cap), DENSE_WARPS * 32, 0, st>>>(a);
