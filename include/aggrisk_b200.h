@@ -44,7 +44,9 @@ typedef enum {
 #define ARE_MAX_TABLES 256 /* reference: _kernel.pyx:14 (MAX_TABLES) */
 
 /* K2 variant selector for are_simulate_* */
-#define ARE_VARIANT_AUTO 0   /* hot-set kernel when zero-skip is exact, else dense */
+#define ARE_VARIANT_AUTO 0   /* hot-set kernel when zero-skip is exact and the plan
+                                is not dense-overlap (>= 3.5 entries per catalog
+                                event, 4-32 rows), else dense */
 #define ARE_VARIANT_HOTSET 1 /* force the hot-set kernel (fails if not exact)      */
 #define ARE_VARIANT_DENSE 2  /* force the dense direct-access kernel              */
 /* OR-able flag: the caller guarantees every event id of the YET is < row_len
