@@ -383,6 +383,13 @@ def price_layer(yet, tset: TableSet, selection: Sequence[int] | None, terms: Lay
 # the resident ids instead of re-streaming them over PCIe (SURVEY.md §8(f)
 # row 1).  Below it the host checks and the per-call stream are cheaper.
 PROMOTE_MIN_OCC = 1 << 24
+# The device copies of the most recently promoted host YETs, keyed by the
+# host object's identity and dropped when it is collected: repeated analyses
+# of one YET (other layers, other terms) upload and validate it once.  Safe
+# because a YET's arrays are read-only (portfolio._frozen; the reference's
+# model.py:186-187 makes the same guarantee).
+PROMOTE_CACHE = 2
+_promoted: dict[int, tuple] = {}
 
 
 def _promote(yet):
@@ -391,6 +398,11 @@ def _promote(yet):
     n = int(yet.offsets[-1]) if yet.offsets.size else 0
     if n < PROMOTE_MIN_OCC or n == 0:
         return yet
+    key = id(yet)
+    hit = _promoted.get(key)
+    if hit is not None and hit[0]() is yet:
+        _promoted[key] = _promoted.pop(key)  # most recent last
+        return hit[1]
     import torch
 
     from .resident import DeviceYearEventTable
@@ -398,7 +410,16 @@ def _promote(yet):
     free, _ = torch.cuda.mem_get_info()
     if 4 * n + 8 * int(yet.offsets.size) > free // 2:  # leave room for tables and outputs
         return yet
-    return DeviceYearEventTable(yet)
+    dyet = DeviceYearEventTable(yet)
+    try:
+        ref = weakref.ref(yet, lambda _r, k=key: _promoted.pop(k, None))
+    except TypeError:  # not weak-referenceable: no caching
+        return dyet
+    dyet.host = weakref.proxy(yet)  # the cache must not keep the host YET alive
+    _promoted[key] = (ref, dyet)
+    while len(_promoted) > PROMOTE_CACHE:
+        _promoted.pop(next(iter(_promoted)))
+    return dyet
 
 
 def run_aggregate_analysis_with_stats(layers: Sequence[Layer], yet, cfg: EngineConfig | None = None,

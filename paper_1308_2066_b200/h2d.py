@@ -39,6 +39,9 @@ class Uploader:
         flat = dst_tensor.view(torch.uint8)
         nbytes = src.nbytes
         raw = src.reshape(-1).view(np.uint8) if src.flags.c_contiguous else np.ascontiguousarray(src).view(np.uint8)
+        # the destination may have been written (e.g. zero-filled) on the
+        # caller's stream: the copies must land after that work
+        self.stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.stream):
             for i, a in enumerate(range(0, nbytes, self.chunk_bytes)):
                 b = min(nbytes, a + self.chunk_bytes)

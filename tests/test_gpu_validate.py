@@ -124,3 +124,30 @@ def test_entry_point_promotes_large_host_yets(monkeypatch, cases):
     (hy, hs), (dy, ds) = host, dev
     assert [y.losses.tobytes() for y in dy] == [y.losses.tobytes() for y in hy]
     assert (ds.trials, ds.layers, ds.lookups) == (hs.trials, hs.layers, hs.lookups)
+
+
+def test_promoted_yet_is_cached_per_host_object(monkeypatch):
+    """Repeated analyses of one large host YET upload and validate it once;
+    the device copy goes when the host YET is collected, and it never keeps
+    the host YET alive."""
+    import gc
+
+    import paper_1308_2066_b200.engine as engine
+
+    monkeypatch.setattr(engine, "PROMOTE_MIN_OCC", 1)
+    yet = _yet("")
+    layers = [_layer()]
+    first = engine.run_aggregate_analysis(layers, yet)
+    d1 = engine._promote(yet)
+    assert engine._promote(yet) is d1 and id(yet) in engine._promoted
+    again = engine.run_aggregate_analysis(layers, yet)
+    assert [y.losses.tobytes() for y in again] == [y.losses.tobytes() for y in first]
+    assert d1.event_ids is yet.event_ids or np.array_equal(d1.event_ids, yet.event_ids)
+    key = id(yet)
+    del yet, d1
+    gc.collect()
+    assert key not in engine._promoted
+    bad = _yet("range")
+    for _ in range(2):  # the cached copy keeps reporting the violation
+        with pytest.raises(PortfolioInvalidError):
+            engine.run_aggregate_analysis(layers, bad)
