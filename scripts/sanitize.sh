@@ -8,3 +8,8 @@ compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test
 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -x -q -k "long_and_ragged or 256_tables" 2>&1 | tail -3
 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -x -q -k "$L" 2>&1 | tail -3
 compute-sanitizer --tool synccheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -x -q -k "long_and_ragged or 256_tables" 2>&1 | tail -3
+# the cooperative event-major dense kernel (k2_dense_coop, one- and two-line strides, FULL and generic shapes)
+D='dense_overlap_plans_event_major_kernel'
+compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -x -q -k "$D" 2>&1 | tail -3
+compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -x -q -k "$D" 2>&1 | tail -3
+compute-sanitizer --tool synccheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -x -q -k "$D" 2>&1 | tail -3
