@@ -349,13 +349,33 @@ def simulate_layers_device(dyet, pool_tset: TableSet, masks, terms_list, out=Non
     return out
 
 
-def _fusable(layers: Sequence[Layer], cfg: EngineConfig):
+# When the entry point fuses layers (the exact kernel; the pre-combined one is
+# an explicit request and always fuses).  The fused pass costs a roughly
+# fixed ~4-5 single-layer runs and grows slowly with the layer count, so it
+# pays from about 5 layers; on dense-overlap pools (the hot set gathers
+# several entries per occurrence for every layer) it loses to per-layer runs
+# of the event-major dense kernel.  Measured, ms per 100k trials x 1000,
+# fused vs per layer (scripts/time_dense_layers.py): 1.5 pool entries per
+# catalog event: 4 layers 6.1 vs 5.3, 8 layers 6.9 vs 10.6; 2.45 entries:
+# 4 layers 9.2 vs 8.2, 8 layers 10.7 vs 16.3; 3.2 entries: 16 layers 21.8 vs
+# 22.3; 6.0 entries: 16 layers 31.4 vs 26.2.
+FUSE_MIN_LAYERS = 5
+FUSE_MAX_ENTRIES_PER_EVENT = 3.0
+
+
+def _fusable(layers: Sequence[Layer], cfg: EngineConfig, catalog_size: int | None = None):
     if len(layers) < 2 or cfg.variant not in ("auto", "hotset"):
+        return None
+    if not cfg.precombine and catalog_size is not None and len(layers) < FUSE_MIN_LAYERS:
         return None
     got = layer_pool(layers)
     if got is None:
         return None
     pool, masks = got
+    if not cfg.precombine and catalog_size:
+        entries = sum(int(np.asarray(e.event_ids).size) for e in pool)
+        if entries > FUSE_MAX_ENTRIES_PER_EVENT * catalog_size:
+            return None
     for e in pool:  # the pool plan must be zero-exact
         t = e.terms
         if not (t.exchange_rate > 0 and math.isfinite(t.exchange_rate) and t.event_retention >= 0
@@ -432,7 +452,7 @@ def run_aggregate_analysis_with_stats(layers: Sequence[Layer], yet, cfg: EngineC
         raise PortfolioInvalidError(violations)
     stats = RunStats(trials=int(yet.offsets.shape[0]) - 1, layers=len(layers))
     ylts: list[YearLossTable] = []
-    fused = _fusable(layers, cfg)
+    fused = _fusable(layers, cfg, int(yet.catalog_size))
     if fused is not None and stats.trials > 0:
         # one pass over the YET for every layer
         from .resident import DeviceYearEventTable

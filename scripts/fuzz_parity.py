@@ -8,7 +8,7 @@ with random occurrence / aggregate terms; then compares, bit for bit:
   * run_aggregate_analysis (auto kernel choice, fused layers when possible),
   * the same with EngineConfig(precombine=True),
   * price_layer per layer with the dense kernel,
-  * a DeviceYearEventTable run,
+  * a DeviceYearEventTable run, and the exact fused layer kernel on it,
 against oracle.run_trials_port per layer; and K3 (PML exact, TVaR rel 1e-12)
 plus the portfolio roll-up on every YLT.
 
@@ -28,7 +28,8 @@ import numpy as np  # noqa: E402
 
 import oracle  # noqa: E402
 from paper_1308_2066_b200.direct_access import TableSet  # noqa: E402
-from paper_1308_2066_b200.engine import EngineConfig, price_layer, run_aggregate_analysis  # noqa: E402
+from paper_1308_2066_b200.engine import (EngineConfig, _fusable, layer_pool, price_layer,  # noqa: E402
+                                         run_aggregate_analysis, simulate_layers_device)
 from paper_1308_2066_b200.errors import PortfolioInvalidError  # noqa: E402
 from paper_1308_2066_b200.portfolio import (EventLossTable, FinancialTerms, Layer, LayerTerms,  # noqa: E402
                                             YearEventTable)
@@ -114,6 +115,12 @@ def main() -> None:
         got = run_aggregate_analysis(layers, dyet)
         for w, g in zip(wants, got):
             assert g.losses.tobytes() == w.tobytes(), (n, "resident")
+        if _fusable(layers, EngineConfig()) is not None:  # the exact fused kernel at any layer count
+            pe, masks = layer_pool(layers)
+            fz = simulate_layers_device(dyet, TableSet.from_elts(pe, yet.catalog_size), masks,
+                                        [lay.terms for lay in layers]).cpu().numpy()
+            for w, g in zip(wants, fz):
+                assert g.tobytes() == w.tobytes(), (n, "fused")
         for lay, w in zip(layers, wants):
             ts = TableSet.from_elts(lay.elts, yet.catalog_size)
             terms = lay.terms

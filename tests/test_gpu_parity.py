@@ -300,9 +300,16 @@ def test_kernel_instantiations_across_hash_modes(catalog):
     got, _ = price_layer(yet, tset, [3, 0, 2], layer.terms, DENSE)
     assert got.tobytes() == _oracle_ylt(sub, yet).tobytes()
     second = Layer("M", tuple(elts[1:3]), LayerTerms(0.0, math.inf, 300.0, 20_000.0))
-    fused = run_aggregate_analysis([layer, second], yet)
-    assert fused[0].losses.tobytes() == want.tobytes()
-    assert fused[1].losses.tobytes() == _oracle_ylt(second, yet).tobytes()
+    want2 = _oracle_ylt(second, yet).tobytes()
+    both = run_aggregate_analysis([layer, second], yet)  # two layers: run singly (FUSE_MIN_LAYERS)
+    assert both[0].losses.tobytes() == want.tobytes() and both[1].losses.tobytes() == want2
+    from paper_1308_2066_b200.engine import layer_pool, simulate_layers_device
+    from paper_1308_2066_b200.resident import DeviceYearEventTable
+
+    pe, masks = layer_pool([layer, second])
+    fused = simulate_layers_device(DeviceYearEventTable(yet), TableSet.from_elts(pe, catalog), masks,
+                                   [layer.terms, second.terms]).cpu().numpy()
+    assert fused[0].tobytes() == want.tobytes() and fused[1].tobytes() == want2
 
 
 def test_256_tables_and_overflow_chains():
