@@ -358,16 +358,24 @@ def simulate_layers_device(dyet, pool_tset: TableSet, masks, terms_list, out=Non
 # fused vs per layer (scripts/time_dense_layers.py): 1.5 pool entries per
 # catalog event: 4 layers 6.1 vs 5.3, 8 layers 6.9 vs 10.6; 2.45 entries:
 # 4 layers 9.2 vs 8.2, 8 layers 10.7 vs 16.3; 3.2 entries: 16 layers 21.8 vs
-# 22.3; 6.0 entries: 16 layers 31.4 vs 26.2.
+# 22.3; 6.0 entries: 16 layers 31.4 vs 26.2.  Below ~5e7 occurrences the
+# per-layer host work (plan build, launch, readback: ~0.3 ms a layer) shifts
+# the crossover to 3 layers (the reference's layer sweep, 20k trials x 1000,
+# 3 ELTs: 3 layers 2.45 ms singly vs ~1.7 ms fused).
 FUSE_MIN_LAYERS = 5
+FUSE_MIN_LAYERS_SMALL = 3
+FUSE_SMALL_OCC = 50_000_000
 FUSE_MAX_ENTRIES_PER_EVENT = 3.0
 
 
-def _fusable(layers: Sequence[Layer], cfg: EngineConfig, catalog_size: int | None = None):
+def _fusable(layers: Sequence[Layer], cfg: EngineConfig, catalog_size: int | None = None,
+             n_occ: int | None = None):
     if len(layers) < 2 or cfg.variant not in ("auto", "hotset"):
         return None
-    if not cfg.precombine and catalog_size is not None and len(layers) < FUSE_MIN_LAYERS:
-        return None
+    if not cfg.precombine and catalog_size is not None:
+        small = n_occ is not None and n_occ < FUSE_SMALL_OCC
+        if len(layers) < (FUSE_MIN_LAYERS_SMALL if small else FUSE_MIN_LAYERS):
+            return None
     got = layer_pool(layers)
     if got is None:
         return None
@@ -452,7 +460,7 @@ def run_aggregate_analysis_with_stats(layers: Sequence[Layer], yet, cfg: EngineC
         raise PortfolioInvalidError(violations)
     stats = RunStats(trials=int(yet.offsets.shape[0]) - 1, layers=len(layers))
     ylts: list[YearLossTable] = []
-    fused = _fusable(layers, cfg, int(yet.catalog_size))
+    fused = _fusable(layers, cfg, int(yet.catalog_size), int(yet.offsets[-1]) if yet.offsets.size else 0)
     if fused is not None and stats.trials > 0:
         # one pass over the YET for every layer
         from .resident import DeviceYearEventTable
