@@ -23,10 +23,12 @@
 //     (each occurrence value added once, in order), exactly like the
 //     reference, so the YLT is bit-identical to the reference kernel; the
 //     skipped +-0 additions cannot change a float64 sum.
-// Dense kernel (k2_dense): the literal per-occurrence loop over every selected
-//   row of the dense float64 tables; used when the zero-skip precondition
-//   does not hold (invalid terms such as negative retentions) and as the
-//   uncompacted comparison point.
+// Dense kernels (k2_dense, k2_dense_coop): the literal per-occurrence loop over
+//   every selected row of the dense float64 tables; used when the zero-skip
+//   precondition does not hold (invalid terms such as negative retentions),
+//   for dense-overlap plans (several table entries per catalog event), and as
+//   the uncompacted comparison point.  From 4 selected rows they read an
+//   event-major copy, eight lanes per event line (k2_dense_coop).
 #include "k2_trials.cuh"
 
 namespace are {
