@@ -229,3 +229,33 @@ def test_layer_pool_orders_and_masks():
     # a layer that orders c before a conflicts with a layer ordering a before c
     assert layer_pool([Layer("x", (a, c)), Layer("y", (c, a))]) is None
     assert layer_pool([Layer("x", (a, a))]) is None
+
+
+def test_entry_point_fusion_rule():
+    """The entry point fuses layers only where the fused pass pays
+    (engine.FUSE_*): enough layers for the trial count, a sparse pool, exact
+    terms; pre-combination always fuses."""
+    from paper_1308_2066_b200 import engine
+    from paper_1308_2066_b200.engine import _fusable
+
+    cat = 1_000
+    rng = np.random.default_rng(3)
+    pool = [EventLossTable(cat, np.sort(rng.choice(np.arange(1, cat + 1), 200, replace=False)).astype(np.uint32),
+                           rng.lognormal(0, 1, 200)) for _ in range(8)]
+    sparse = [Layer(f"s{i}", tuple(pool[:4]), LayerTerms(float(i), 1e6)) for i in range(6)]  # 0.8 entries/event
+    dense = [Layer(f"d{i}", tuple(pool), LayerTerms(float(i), 1e6)) for i in range(6)]        # 1.6 entries/event
+    cfg, pre = EngineConfig(), EngineConfig(precombine=True)
+    big, small = 10 ** 9, 10 ** 6
+    assert _fusable(sparse, cfg) is not None                     # no size information: fusable
+    assert _fusable(sparse[:4], cfg, cat, big) is None           # < FUSE_MIN_LAYERS at scale
+    assert _fusable(sparse[:4], cfg, cat, small) is not None     # small runs fuse from 3 layers
+    assert _fusable(sparse[:2], cfg, cat, small) is None
+    assert _fusable(sparse, cfg, cat, big) is not None
+    assert _fusable(dense, cfg, cat, big) is not None            # 1.6 <= FUSE_MAX_ENTRIES_PER_EVENT
+    assert _fusable(dense, cfg, cat // 2, big) is None           # 3.2 entries per catalog event
+    assert _fusable(dense, pre, cat // 2, big) is not None       # explicit pre-combination
+    assert _fusable(sparse[:2], pre, cat, big) is not None
+    assert _fusable(sparse, EngineConfig(variant="dense"), cat, big) is None
+    neg = sparse[:5] + [Layer("neg", tuple(pool[:4]), LayerTerms(-1.0, 1e6))]
+    assert _fusable(neg, cfg, cat, big) is None                  # not zero-exact: layers run singly
+    assert engine.FUSE_MIN_LAYERS_SMALL <= engine.FUSE_MIN_LAYERS
