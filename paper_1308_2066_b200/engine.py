@@ -417,7 +417,7 @@ PROMOTE_MIN_OCC = 1 << 24
 # because a YET's arrays are read-only (portfolio._frozen; the reference's
 # model.py:186-187 makes the same guarantee).
 PROMOTE_CACHE = 2
-_promoted: dict[int, tuple] = {}
+_promoted: dict[tuple, tuple] = {}  # (id(host YET), device) -> (weakref, DeviceYearEventTable)
 
 
 def _promote(yet):
@@ -426,12 +426,13 @@ def _promote(yet):
     n = int(yet.offsets[-1]) if yet.offsets.size else 0
     if n < PROMOTE_MIN_OCC or n == 0:
         return yet
-    key = id(yet)
+    import torch
+
+    key = (id(yet), torch.cuda.current_device())  # a copy serves the device it lives on
     hit = _promoted.get(key)
     if hit is not None and hit[0]() is yet:
         _promoted[key] = _promoted.pop(key)  # most recent last
         return hit[1]
-    import torch
 
     from .resident import DeviceYearEventTable
 
