@@ -29,3 +29,14 @@ def test_parity_suite_under_each_kernel(force):
                         "-x", "-p", "no:cacheprovider", "-k", CASES], cwd=ROOT, env=env, capture_output=True,
                        text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_dense_suite_under_lane_per_line_kernel():
+    """ARE_DENSE_COOP=0 runs the lane-per-line event-major dense kernel
+    (k2_dense<EM>) in place of the cooperative one: the dense parity tests
+    under it, so the A/B path stays bit-exact too."""
+    env = dict(os.environ, ARE_DENSE_COOP="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-q",
+                        "-x", "-p", "no:cacheprovider", "-k", "dense or degenerate or instantiations or 256_tables"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
