@@ -151,3 +151,22 @@ def test_promoted_yet_is_cached_per_host_object(monkeypatch):
     for _ in range(2):  # the cached copy keeps reporting the violation
         with pytest.raises(PortfolioInvalidError):
             engine.run_aggregate_analysis(layers, bad)
+
+
+def test_k0_reports_equal_reference_fixture(tmp_path):
+    """K0 (DeviceYearEventTable) and the ARE1 -> HBM loader produce the
+    reference's own validate_portfolio report (model.py:360-404) byte for
+    byte on the 169 reference-written cases (tests/golden/validation.json.gz,
+    tests/golden/make_validation.py) -- not just the repo's host restatement."""
+    from tests.validation_cases import build, load_cases
+
+    for i, case in enumerate(load_cases()):
+        layers, yet = build(case)
+        dyet = DeviceYearEventTable(yet)
+        got = [str(v) for v in validate_portfolio(layers, dyet)]
+        assert got == case["report"], case["name"]
+        if yet.offsets.size > 1 and i % 4 == 0:  # the direct file loader on a quarter of them
+            path = tmp_path / f"c{i}.are1"
+            save_yet(yet, path)
+            got = [str(v) for v in validate_portfolio(layers, load_yet_device(path, chunk=7))]
+            assert got == case["report"], case["name"] + " (ARE1)"

@@ -259,3 +259,21 @@ def test_entry_point_fusion_rule():
     neg = sparse[:5] + [Layer("neg", tuple(pool[:4]), LayerTerms(-1.0, 1e6))]
     assert _fusable(neg, cfg, cat, big) is None                  # not zero-exact: layers run singly
     assert engine.FUSE_MIN_LAYERS_SMALL <= engine.FUSE_MIN_LAYERS
+
+
+# ------------------------------------- validation pinned to the reference --
+
+def test_validation_report_equals_reference_fixture():
+    """Byte-equal `[category] message` lists against the reference's own
+    validate_portfolio (model.py:360-404) on 169 cases: its per-category
+    tests (pkg/tests/test_model.py:138-258), NaN timestamps, id 0, empty and
+    over-long trials, boundary drops, combined faults and a seeded random mix
+    (tests/golden/make_validation.py)."""
+    from tests.validation_cases import build, load_cases
+
+    cases = load_cases()
+    assert len(cases) >= 150
+    for case in cases:
+        layers, yet = build(case)
+        got = [str(v) for v in validate_portfolio(layers, yet)]
+        assert got == case["report"], case["name"]
