@@ -57,6 +57,7 @@ typedef enum {
 typedef struct are_tables_s *are_tables_t;
 typedef struct are_plan_s *are_plan_t;
 typedef struct are_layer_table_s *are_layer_table_t;
+typedef struct are_yet_s *are_yet_t;
 
 typedef struct {
     int64_t n_sel;            /* selected tables (accumulation order)            */
@@ -225,6 +226,56 @@ int are_order_stats_host(const double *losses, int64_t n,
 /* portfolio_rollup (metrics.py:118-133): d_out[t] = ((y0[t] + y1[t]) + ...). */
 int are_rollup_device(const double *const *d_ylts, int64_t n_layers, int64_t n,
                       double *d_out, void *stream);
+
+
+/* ---- multi-GPU group ----------------------
+ * Replaces the reference's worker pool over trial ranges
+ * (pkg/src/aggrisk/engine/__init__.py:193-200, _split_by_events :151-159):
+ * a request with worker_count > 1 becomes ONE call covering every GPU of the
+ * group.  The caller computes the trial -> GPU partition with the reference
+ * rule (split_by_events(offsets, G)) and passes it as `bounds` (G + 1 trial
+ * cut points); shard s lives on group member s.  Tables are replicated
+ * (are_tables_replicate) and planned per GPU; plans[s] must live on shard
+ * s's GPU.  Every trial is computed by one warp on one GPU, so the YLT is
+ * bit-identical for any group size.  Handles are thread-safe; one layer run
+ * at a time per YET handle (internal mutex). */
+/* Group = CUDA devices 0..n_gpus-1 (n_gpus <= 0: every visible device). */
+int are_init(int n_gpus);
+/* Group of explicit ordinals (a device may repeat: several shards on one GPU). */
+int are_init_devices(const int *ordinals, int32_t n);
+int are_shutdown(void);
+int are_group_size(int32_t *n);
+int are_group_device(int32_t member, int *ordinal);
+int are_tables_device(are_tables_t t, int *device);
+int are_plan_device(are_plan_t p, int *device);
+/* Copy a table set into another GPU's memory (peer copy). */
+int are_tables_replicate(are_tables_t t, int device, are_tables_t *out);
+/* Host YET -> HBM, one shard per group member (uploaded concurrently, pinned
+ * staging for pageable inputs), validated on the device by K0: ids, trial
+ * lengths in [1, max_len] and, when `timestamps` is non-null, the timestamp
+ * checks of validate_portfolio (model.py:371-395).  The merged report is
+ * read with are_yet_report. */
+int are_yet_upload(const uint32_t *ids, int64_t n_occ, const int64_t *offsets, int64_t n_trials,
+                   const double *timestamps, const int64_t *bounds, int32_t n_shards, int64_t max_len,
+                   are_yet_t *out);
+int are_yet_report(are_yet_t y, are_yet_report_t *out);
+int are_yet_shards(are_yet_t y, int32_t *n_shards, int64_t *bounds, int *devices);
+int are_yet_free(are_yet_t y);
+/* K2 over trials [first, last) on every shard's GPU at once (the reference's
+ * _run_layer, engine/__init__.py:162-201); out_host[t] for t in range,
+ * *lookups = n_sel * occurrences.  With n_rp > 0 (whole table only) the
+ * slices are also gathered into the first member's HBM (peer copies) and K3
+ * evaluates pml/tvar there (metrics.py:29-63).  out_host may be NULL. */
+int are_run_layer(are_yet_t y, const are_plan_t *plans, int32_t n_plans,
+                  double occ_ret, double occ_lim, double agg_ret, double agg_lim,
+                  int64_t first, int64_t last, double *out_host, int64_t *lookups, int32_t variant,
+                  const double *rps, int64_t n_rp, double *pml_out, double *tvar_out);
+/* Host-YET form: shard s streams its trials to its GPU over that GPU's own
+ * PCIe link (are_simulate_host per shard, concurrently). */
+int are_run_layer_host(const uint32_t *ids, int64_t n_occ, const int64_t *offsets, int64_t n_trials,
+                       const int64_t *bounds, int32_t n_shards, const are_plan_t *plans,
+                       double occ_ret, double occ_lim, double agg_ret, double agg_lim,
+                       int64_t first, int64_t last, double *out, int64_t *lookups, int32_t variant);
 
 #ifdef __cplusplus
 }

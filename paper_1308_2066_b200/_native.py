@@ -103,6 +103,23 @@ SIGNATURES = {
     "are_order_stats_device": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _P]),
     "are_order_stats_host": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P]),
     "are_rollup_device": (ctypes.c_int, [_P, _I64, _I64, _P, _P]),
+    # multi-GPU group (capi_group.cu)
+    "are_init": (ctypes.c_int, [ctypes.c_int]),
+    "are_init_devices": (ctypes.c_int, [_P, _I32]),
+    "are_shutdown": (ctypes.c_int, []),
+    "are_group_size": (ctypes.c_int, [ctypes.POINTER(_I32)]),
+    "are_group_device": (ctypes.c_int, [_I32, ctypes.POINTER(ctypes.c_int)]),
+    "are_tables_device": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int)]),
+    "are_plan_device": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int)]),
+    "are_tables_replicate": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_P)]),
+    "are_yet_upload": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _I32, _I64, ctypes.POINTER(_P)]),
+    "are_yet_report": (ctypes.c_int, [_P, ctypes.POINTER(YetReport)]),
+    "are_yet_shards": (ctypes.c_int, [_P, ctypes.POINTER(_I32), _P, _P]),
+    "are_yet_free": (ctypes.c_int, [_P]),
+    "are_run_layer": (ctypes.c_int, [_P, _P, _I32, _D, _D, _D, _D, _I64, _I64, _P, ctypes.POINTER(_I64), _I32,
+                                     _P, _I64, _P, _P]),
+    "are_run_layer_host": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _I32, _P, _D, _D, _D, _D, _I64, _I64, _P,
+                                          ctypes.POINTER(_I64), _I32]),
 }
 
 _lock = threading.Lock()
@@ -216,6 +233,18 @@ def plan_build(tables: Handle, rows, rate, ret, lim, share, pool: bool = False,
     fn = lib.are_plan_build_pool if pool else (lib.are_plan_build_precombined if precombine else lib.are_plan_build)
     check(fn(tables.value, ptr(arrs[0]), arrs[0].shape[0], *(ptr(x) for x in arrs[1:]), ctypes.byref(out)))
     return Handle(out.value, "are_plan_free")
+
+
+def tables_device(tables: Handle) -> int:
+    d = ctypes.c_int(0)
+    check(load().are_tables_device(tables.value, ctypes.byref(d)))
+    return int(d.value)
+
+
+def tables_replicate(tables: Handle, device: int) -> Handle:
+    out = _P()
+    check(load().are_tables_replicate(tables.value, int(device), ctypes.byref(out)))
+    return Handle(out.value, "are_tables_free")
 
 
 def plan_info(plan: Handle) -> PlanInfo:

@@ -16,6 +16,7 @@
 #include "k1_ingest.cuh"
 #include "k2_trials.cuh"
 #include "k3_order_stats.cuh"
+#include "capi_internal.cuh"
 
 namespace are {
 
@@ -33,15 +34,10 @@ int cuda_fail(cudaError_t e, const char *what) {
 }
 
 // ---- per-device facts ------------------------------------------------------
-struct DeviceInfo {
-    int sms = 0;
-    int smem_optin = 0;
-    bool ready = false;
-};
 static std::mutex g_dev_mu;
 static DeviceInfo g_dev[64];
 
-static int use_device(int dev, DeviceInfo **out) {
+int use_device(int dev, DeviceInfo **out) {
     if (dev < 0 || dev >= 64) return fail(ARE_EINVAL, "bad device ordinal");
     ARE_CUDA(cudaSetDevice(dev));
     std::lock_guard<std::mutex> g(g_dev_mu);
@@ -70,37 +66,8 @@ static int current_device(int *dev) {
 
 using namespace are;
 
-struct are_tables_s {
-    int device = 0;
-    int64_t n_tables = 0, row_len = 0;
-    double *d = nullptr;
-    std::atomic<int> refs{1};
-};
-
-struct are_plan_s {
-    int device = 0;
-    are_tables_s *tab = nullptr;
-    int64_t n_sel = 0;
-    int64_t *d_rows = nullptr;
-    Fin *d_fin = nullptr;
-    PlanBuffers pb;
-    int64_t nbits = 0;
-    int hash_mode = 0;
-    bool zero_skip = false;
-    bool slot0_hot = false;
-    bool pool = false;
-    bool precombined = false;
-    unsigned int *d_err = nullptr;
-    size_t smem = 0;
-    // event-major copy of the selected rows for the dense kernel (built on
-    // its first use; n_sel <= EM_MAX_SEL)
-    std::mutex em_mu;
-    double *d_em = nullptr;
-    int32_t em_stride = 0;
-    bool em_tried = false;
-};
-
 static void tables_release(are_tables_s *t) {
+    DeviceGuard dg;
     if (t && t->refs.fetch_sub(1) == 1) {
         cudaSetDevice(t->device);
         cudaFree(t->d);
@@ -129,7 +96,7 @@ static constexpr int64_t CHUNK_OCC = 32ll << 20;  // 32 Mi occurrences (128 MiB 
 
 // Host -> pinned staging copy on several threads: one thread copies pageable
 // memory at ~10-14 GB/s, well below the PCIe rate the copy engine drains it at.
-static void parallel_copy(void *dst, const void *src, size_t bytes) {
+void parallel_copy(void *dst, const void *src, size_t bytes) {
     constexpr size_t MIN_PIECE = 8u << 20;
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     const size_t n = std::min<size_t>(std::min<size_t>(hw, 16), std::max<size_t>(1, bytes / MIN_PIECE));
@@ -199,7 +166,7 @@ static int ws_reserve(Workspace &w, int64_t ids, int64_t offs, int64_t outs, boo
     return ARE_OK;
 }
 
-static bool is_pinned(const void *p) {
+bool is_pinned(const void *p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
@@ -311,6 +278,35 @@ static void fill_args(const are_plan_s *p, K2Args &a, double occ_ret, double occ
     a.precombined = p->precombined ? 1 : 0;
     a.em = p->d_em;
     a.em_stride = p->em_stride;
+}
+
+// K2 over trials [first, last) of ids/offsets indexed from id_base/t_base
+// (ids[i - id_base] is occurrence i, off[t - t_base] is offset t) into
+// out[t - out_base]; launches on `st`, no synchronisation.  Shared by the
+// single-device entry points and the multi-GPU group (capi_group.cu).
+int simulate_range(are_plan_s *p, const uint32_t *ids, int64_t id_base, int64_t n_ids, const int64_t *off,
+                   int64_t t_base, int64_t first, int64_t last, double mean_len, double occ_ret, double occ_lim,
+                   double agg_ret, double agg_lim, double *out, int64_t out_base, unsigned int *d_err,
+                   cudaStream_t st, int32_t variant) {
+    int v, rc;
+    if ((rc = choose_variant(p, occ_ret, occ_lim, variant, &v))) return rc;
+    DeviceInfo *di;
+    if ((rc = use_device(p->device, &di))) return rc;
+    if ((v & 0xFF) == ARE_VARIANT_DENSE && (rc = ensure_event_major(p, di->sms, st))) return rc;
+    K2Args a{};
+    fill_args(p, a, occ_ret, occ_lim, agg_ret, agg_lim);
+    a.mean_len = mean_len;
+    a.ids = ids;
+    a.id_base = id_base;
+    a.n_ids = n_ids;
+    a.offsets = off;
+    a.t_base = t_base;
+    a.first = first;
+    a.last = last;
+    a.out = out;
+    a.out_base = out_base;
+    a.err = d_err ? d_err : p->d_err;
+    return k2_launch(a, v, di->sms, p->smem, st);
 }
 
 }  // namespace are
@@ -464,6 +460,7 @@ int are_tables_info(are_tables_t t, int64_t *n_tables, int64_t *row_len, int64_t
 }
 
 int are_tables_read_row(are_tables_t t, int64_t row, double *host_out) {
+    DeviceGuard dg;
     if (!t) return fail(ARE_EINVAL, "null tables handle");
     if (row < 0 || row >= t->n_tables) return fail(ARE_EINDEX, "table row out of range");
     ARE_CUDA(cudaSetDevice(t->device));
@@ -480,6 +477,7 @@ int are_tables_free(are_tables_t t) {
 static int plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
                       const double *fin_ret, const double *fin_lim, const double *fin_share, bool pool,
                       bool precombine, are_plan_t *out) {
+    DeviceGuard dg;
     if (!t) return fail(ARE_EINVAL, "null tables handle");
     if (n_sel < 1) return fail(ARE_EINVAL, "table selection is empty");
     if (n_sel > ARE_MAX_TABLES)
@@ -552,17 +550,20 @@ static int plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const 
 
 int are_plan_build(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
                    const double *fin_ret, const double *fin_lim, const double *fin_share, are_plan_t *out) {
+    DeviceGuard dg;
     return plan_build(t, rows, n_sel, fin_rate, fin_ret, fin_lim, fin_share, false, false, out);
 }
 
 int are_plan_build_precombined(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
                                const double *fin_ret, const double *fin_lim, const double *fin_share,
                                are_plan_t *out) {
+    DeviceGuard dg;
     return plan_build(t, rows, n_sel, fin_rate, fin_ret, fin_lim, fin_share, false, true, out);
 }
 
 int are_plan_build_pool(are_tables_t t, const int64_t *rows, int64_t n_sel, const double *fin_rate,
                         const double *fin_ret, const double *fin_lim, const double *fin_share, are_plan_t *out) {
+    DeviceGuard dg;
     return plan_build(t, rows, n_sel, fin_rate, fin_ret, fin_lim, fin_share, true, false, out);
 }
 
@@ -582,6 +583,7 @@ int are_plan_info(are_plan_t p, are_plan_info_t *info) {
 }
 
 int are_plan_free(are_plan_t p) {
+    DeviceGuard dg;
     if (!p) return ARE_OK;
     cudaSetDevice(p->device);
     cudaFree(p->d_rows);
@@ -600,6 +602,7 @@ int are_plan_free(are_plan_t p) {
 int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ, const int64_t *d_offsets,
                         int64_t n_trials, int64_t first, int64_t last, double occ_ret, double occ_lim,
                         double agg_ret, double agg_lim, double *d_out, void *stream, int32_t variant) {
+    DeviceGuard dg;
     if (!p) return fail(ARE_EINVAL, "null plan handle");
     if (first < 0 || last < first || last > n_trials) return fail(ARE_EINVAL, "trial range out of bounds");
     int v, rc;
@@ -676,6 +679,7 @@ int are_simulate_layers_device(are_plan_t p, int32_t n_layers, const uint64_t *m
                                const uint32_t *d_event_ids, int64_t n_occ, const int64_t *d_offsets, int64_t n_trials,
                                int64_t first, int64_t last, double *d_out, int64_t out_stride, void *stream,
                                int32_t flags) {
+    DeviceGuard dg;
     std::vector<LayerTerm> lt;
     int rc;
     if ((rc = layer_terms_check(p, n_layers, masks, layer_terms, lt))) return rc;
@@ -700,6 +704,7 @@ int are_simulate_layers_device(are_plan_t p, int32_t n_layers, const uint64_t *m
 
 int are_layer_table_build(are_plan_t p, int32_t n_layers, const uint64_t *masks, const double *layer_terms,
                           void *stream, are_layer_table_t *out) {
+    DeviceGuard dg;
     if (!out) return fail(ARE_EINVAL, "null output handle");
     *out = nullptr;
     std::vector<LayerTerm> lt;
@@ -739,6 +744,7 @@ int are_layer_table_build(are_plan_t p, int32_t n_layers, const uint64_t *masks,
 }
 
 int are_layer_table_free(are_layer_table_t t) {
+    DeviceGuard dg;
     if (!t) return ARE_OK;
     cudaFree(t->d_masks);
     cudaFree(t->d_terms);
@@ -750,6 +756,7 @@ int are_layer_table_free(are_layer_table_t t) {
 int are_simulate_layers_precombined(are_layer_table_t t, const uint32_t *d_event_ids, int64_t n_occ,
                                     const int64_t *d_offsets, int64_t n_trials, int64_t first, int64_t last,
                                     double *d_out, int64_t out_stride, void *stream, int32_t flags) {
+    DeviceGuard dg;
     if (!t) return fail(ARE_EINVAL, "null layer table handle");
     if (first < 0 || last < first || last > n_trials) return fail(ARE_EINVAL, "trial range out of bounds");
     are_plan_s *p = t->plan;
@@ -763,6 +770,7 @@ int are_simulate_layers_precombined(are_layer_table_t t, const uint32_t *d_event
 }
 
 int are_check_errors(are_plan_t p, void *stream) {
+    DeviceGuard dg;
     if (!p) return fail(ARE_EINVAL, "null plan handle");
     ARE_CUDA(cudaSetDevice(p->device));
     unsigned int h = 0;
@@ -780,6 +788,7 @@ int are_check_errors(are_plan_t p, void *stream) {
 int are_simulate_host(are_plan_t p, const uint32_t *event_ids, int64_t n_occ, const int64_t *offsets,
                       int64_t n_trials, int64_t first, int64_t last, double occ_ret, double occ_lim,
                       double agg_ret, double agg_lim, double *out, int64_t *lookups, int32_t variant) {
+    DeviceGuard dg;
     if (!p) return fail(ARE_EINVAL, "null plan handle");
     if (first < 0 || last < first || last > n_trials) return fail(ARE_EINVAL, "trial range out of bounds");
     if (offsets[n_trials] > n_occ) return fail(ARE_EINVAL, "offsets exceed the occurrence count");

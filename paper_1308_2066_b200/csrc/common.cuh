@@ -70,6 +70,25 @@ __device__ __forceinline__ double fin_term(const Fin &f, double x) {
     double l = __dsub_rn(__dmul_rn(f.rate, x), f.ret);
     return __dmul_rn(f.share, clamp_ref(l, f.lim));
 }
+// Financial terms as four shared-memory arrays (structure of arrays: rate[n],
+// ret[n], lim[n], share[n]).  A warp whose lanes evaluate different tables
+// reads four 8-byte words per lane from four <= n-word rows, which the
+// shared-memory crossbar serves in one or two wavefronts each; the 32-byte
+// Fin struct read as two LDS.128 by lanes with different j costs ~9 wavefronts
+// each (ncu, profiles/r02_k2_lsu.md).
+__device__ __forceinline__ void fin_soa_store(double *s, int n, const Fin *g) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const Fin f = g[i];
+        s[i] = f.rate;
+        s[n + i] = f.ret;
+        s[2 * n + i] = f.lim;
+        s[3 * n + i] = f.share;
+    }
+}
+__device__ __forceinline__ double fin_term_soa(const double *s, int n, uint32_t j, double x) {
+    double l = __dsub_rn(__dmul_rn(s[j], x), s[n + j]);
+    return __dmul_rn(s[3 * n + j], clamp_ref(l, s[2 * n + j]));
+}
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
@@ -103,6 +122,12 @@ __device__ __forceinline__ uint32_t ld_stream_if(const uint32_t *p, uint32_t rel
         : "+r"(r)
         : "r"(rel), "r"(len), "l"(p), "l"(policy));
     return r;
+}
+// Bulk L2 prefetch (cp.async.bulk.prefetch, TMA unit): `bytes` (multiple of
+// 16) from a 16-byte aligned global address into L2, no registers or shared
+// memory held while it is in flight.
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;

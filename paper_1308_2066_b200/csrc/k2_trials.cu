@@ -34,6 +34,34 @@
 namespace are {
 
 static constexpr int QCAP = 128;  // per-warp hot queue: < 32 pending + 2 rows of 32
+// Build-time variants of k2_hotset (A/B experiments; the defaults are the
+// measured choice).
+#ifndef ARE_K2_FIN_SOA
+#define ARE_K2_FIN_SOA 1      // financial terms as four shared arrays
+#endif
+#ifndef ARE_K2_VRING
+#define ARE_K2_VRING 0        // fold only non-zero values, from a per-warp ring (measured slower)
+#endif
+#ifndef ARE_K2_FILTER_FIRST
+#define ARE_K2_FILTER_FIRST 1 // the filter at shared offset 0
+#endif
+#ifndef ARE_K2_FOLD_LANE0
+#define ARE_K2_FOLD_LANE0 1   // fold on lane 0 only
+#endif
+#ifndef ARE_K2_INTERIOR
+#define ARE_K2_INTERIOR 1     // unpredicated id loads for chunks inside the trial
+#endif
+#ifndef ARE_K2_L2PF
+#define ARE_K2_L2PF 4         // bulk L2 prefetch of the id chunk this many chunks ahead (0: off)
+#endif
+#if ARE_K2_FIN_SOA
+#define FIN_TERM(j, x) fin_term_soa(s_fs, nsel, (j), (x))
+#else
+#define FIN_TERM(j, x) fin_term(reinterpret_cast<const Fin *>(s_fs)[(j)], (x))
+#endif
+// per-warp value buffer: the ring of non-zero occurrence values (< 32
+// unfolded + one batch), or one batch of values when the ring is off
+static constexpr int VRING = ARE_K2_VRING ? 64 : 32;
 
 // Event id -> filter bit.  HASH 0: the filter covers the catalog (exact);
 // 1: catalog <= 2 * nbits, fold once (min picks e - nbits iff e >= nbits,
@@ -51,19 +79,32 @@ __device__ __forceinline__ uint32_t hot_hash(uint32_t e, uint32_t nbits) {
 // kept in flight.  Filter hits are appended, in trial order, to the warp's
 // queue; every 32 queued events form one batch: lane i gathers the record of
 // the i-th event, applies the financial and occurrence terms, and the warp
-// folds the 32 occurrence values into c strictly in order.
+// folds the occurrence values into c strictly in order.
 // CHECK = false when the caller has validated every id <= catalog (the
 // reference's validate_portfolio, or DeviceYearEventTable's upload check).
 template <int HASH, bool CHECK, bool PRE>
 __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
     constexpr int NW = K2_THREADS / 32;
     extern __shared__ __align__(16) unsigned char smem[];
-    Fin *s_fin = reinterpret_cast<Fin *>(smem);
-    double *s_occ = reinterpret_cast<double *>(smem + a.fin_bytes);
-    uint32_t *s_q = reinterpret_cast<uint32_t *>(s_occ + NW * 32);
+#if ARE_K2_FILTER_FIRST
+    // the filter at offset 0 (its LDS addresses need no base register); the
+    // queues, value buffers and terms after it
+    uint32_t *s_filter = reinterpret_cast<uint32_t *>(smem);
+    uint32_t *s_q = s_filter + a.filter_words;
+    double *s_val = reinterpret_cast<double *>(s_q + NW * QCAP);           // per-warp value buffers
+    double *s_fs = s_val + NW * VRING;                                     // financial terms
+#else
+    double *s_fs = reinterpret_cast<double *>(smem);                      // financial terms
+    double *s_val = reinterpret_cast<double *>(smem + a.fin_bytes);        // per-warp value buffers
+    uint32_t *s_q = reinterpret_cast<uint32_t *>(s_val + NW * VRING);
     uint32_t *s_filter = s_q + NW * QCAP;
+#endif
 
-    for (int i = threadIdx.x; i < a.n_sel; i += blockDim.x) s_fin[i] = a.fin[i];
+#if ARE_K2_FIN_SOA
+    fin_soa_store(s_fs, a.n_sel, a.fin);
+#else
+    for (int i = threadIdx.x; i < a.n_sel; i += blockDim.x) reinterpret_cast<Fin *>(s_fs)[i] = a.fin[i];
+#endif
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(a.filter);
         uint4 *dst = reinterpret_cast<uint4 *>(s_filter);
@@ -73,8 +114,8 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double *ob = s_occ + warp * 32;
-    const double2 *ob2 = reinterpret_cast<const double2 *>(ob);
+    const int nsel = a.n_sel;
+    double *vr = s_val + warp * VRING;
     uint32_t *q = s_q + warp * QCAP;
     const uint32_t q_saddr = (uint32_t)__cvta_generic_to_shared(q);
     const uint32_t lt = lanemask_lt();
@@ -89,36 +130,71 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
 
     // A batch is 32 queued events, one per lane.  It runs in two halves so
     // the record gathers of batch j are in flight while batch j-1 is finished
-    // (terms + in-order fold) and while the next rows are filtered.
+    // (terms, then its non-zero occurrence values appended in order to the
+    // warp's value ring) and while the next rows are filtered.  The ring is
+    // folded into c strictly in order, 32 values at a time: a value that is
+    // +-0 is never appended (c >= +0, so adding it is an exact no-op), which
+    // skips the ~45% of queued events that are filter false positives or fall
+    // below the occurrence retention.
+    uint32_t vh = 0, vt = 0;  // value ring head / tail (uniform); vh % 32 == 0
     auto finish = [&](const Slot &s, uint32_t n, double &c) {
-        // lane's event: financial terms in selection order, occurrence terms
+        double v = 0.0;
         if ((uint32_t)lane < n) {
             const uint32_t cnt = s.meta >> 16;
             double comb = 0.0;
             if (PRE) {  // pre-combined plan: x already holds comb
                 if (cnt) comb = s.x;
             } else {
-                if (cnt) comb = __dadd_rn(0.0, fin_term(s_fin[s.meta & 0xFFFFu], s.x));
+                if (cnt) comb = __dadd_rn(0.0, FIN_TERM(s.meta & 0xFFFFu, s.x));
 #pragma unroll 1
                 for (uint32_t i = 1; i < cnt; ++i) {  // events in several tables (~7%)
                     const Entry en = a.ovf[s.ovf + i - 1];
-                    comb = __dadd_rn(comb, fin_term(s_fin[en.j], en.x));
+                    comb = __dadd_rn(comb, FIN_TERM(en.j, en.x));
                 }
             }
-            ob[lane] = clamp_ref(__dsub_rn(comb, occ_ret), occ_lim);
+            v = clamp_ref(__dsub_rn(comb, occ_ret), occ_lim);
+        }
+#if !ARE_K2_VRING
+        // every value of the batch in order (zeros included), as the reference adds them
+        vr[lane] = v;
+        __syncwarp();
+#if ARE_K2_FOLD_LANE0
+        // only lane 0 needs c (it writes the trial's result): a one-lane
+        // LDS.128 is one shared-memory wavefront, a 32-lane broadcast two
+        if (lane == 0)
+#endif
+        {
+            if (n == 32) {
+                const double2 *r2 = reinterpret_cast<const double2 *>(vr);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const double2 w = r2[i];
+                    c = __dadd_rn(c, w.x);
+                    c = __dadd_rn(c, w.y);
+                }
+            } else {
+                for (uint32_t i = 0; i < n; ++i) c = __dadd_rn(c, vr[i]);
+            }
         }
         __syncwarp();
-        if (n == 32) {
+        return;
+#endif
+        const bool keep = !(v == 0.0);  // NaN is kept, +-0 skipped
+        const uint32_t b = ballot_full(keep);
+        if (keep) vr[(vt + __popc(b & lt)) & (VRING - 1)] = v;
+        vt += __popc(b);
+        __syncwarp();
+        if (vt - vh >= 32u) {
+            const double2 *r2 = reinterpret_cast<const double2 *>(vr + (vh & (VRING - 1)));
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-                const double2 v = ob2[i];
-                c = __dadd_rn(c, v.x);
-                c = __dadd_rn(c, v.y);
+                const double2 w = r2[i];
+                c = __dadd_rn(c, w.x);
+                c = __dadd_rn(c, w.y);
             }
-        } else {
-            for (uint32_t i = 0; i < n; ++i) c = __dadd_rn(c, ob[i]);
+            vh += 32u;
+            __syncwarp();
         }
-        __syncwarp();
     };
     auto gather = [&](uint32_t qh, uint32_t n) -> Slot {
         Slot s{0.0, 0u, 0u};
@@ -150,6 +226,8 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
         const int nchunks = (int)((len + skew + 127) >> 7);
         double c = 0.0;
         uint32_t qh = 0, qt = 0;
+        vh = 0;
+        vt = 0;
         bool pending = false;  // a gathered, unfinished batch (uniform)
         Slot ps{0.0, 0u, 0u};
 
@@ -162,8 +240,28 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
         for (int k = 0; k < 4; ++k) r1[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream, pad);
 
         auto step = [&](uint32_t (&cur)[4], uint32_t (&fut)[4]) {
+#if ARE_K2_L2PF
+            // the chunk ARE_K2_L2PF ahead goes to L2 now (one bulk request by
+            // lane 0), so its row loads two chunks from now hit L2, not DRAM
+            if (lane == 0) {
+                const uint32_t ahead = rel - (uint32_t)lane + 128u * ARE_K2_L2PF;  // relative start of that chunk
+                if ((int32_t)ahead < (int32_t)len) prefetch_l2_bulk(p - lane + 128 * ARE_K2_L2PF, 512);
+            }
+#endif
+#if ARE_K2_INTERIOR
+            // a chunk wholly inside the trial loads without predicates (uniform test)
+            const uint32_t rel0 = rel - (uint32_t)lane + 256u;  // chunk start relative to the trial
+            if ((int32_t)rel0 >= 0 && rel0 + 128u <= len) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) fut[k] = ld_stream_u32(p + 256 + 32 * k, pol_stream);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 256 + 32 * k, rel + 256 + 32 * k, len, pol_stream, pad);
+            }
+#else
 #pragma unroll
             for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 256 + 32 * k, rel + 256 + 32 * k, len, pol_stream, pad);
+#endif
             // filter words for all four rows first (independent shared loads)
             uint32_t ev[4], word[4];
 #pragma unroll
@@ -209,6 +307,20 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
         const Slot ns = gather(qh, n);
         if (pending) finish(ps, 32u, c);
         if (n) finish(ns, n, c);
+#if ARE_K2_VRING
+        {  // the ring's last (< 32) values, in order
+            const uint32_t m = vt - vh;
+            const double *r = vr + (vh & (VRING - 1));
+            uint32_t i = 0;
+            for (; i + 1 < m; i += 2) {
+                const double2 w = *reinterpret_cast<const double2 *>(r + i);
+                c = __dadd_rn(c, w.x);
+                c = __dadd_rn(c, w.y);
+            }
+            if (i < m) c = __dadd_rn(c, r[i]);
+            __syncwarp();
+        }
+#endif
         if (lane == 0) a.out[t - a.out_base] = clamp_ref(__dsub_rn(c, a.agg_ret), a.agg_lim);
         lo = nlo;
         hi = nhi;
@@ -232,12 +344,12 @@ template <int HASH, bool CHECK, bool PRE>
 __global__ void __launch_bounds__(K2_THREADS, 1) k2_pair(const K2Args a) {
     constexpr int NW = K2_THREADS / 32;
     extern __shared__ __align__(16) unsigned char smem[];
-    Fin *s_fin = reinterpret_cast<Fin *>(smem);
+    double *s_fs = reinterpret_cast<double *>(smem);  // financial terms, SoA
     double *s_occ = reinterpret_cast<double *>(smem + a.fin_bytes);
-    uint32_t *s_q = reinterpret_cast<uint32_t *>(s_occ + NW * 32);
+    uint32_t *s_q = reinterpret_cast<uint32_t *>(s_occ + NW * VRING);  // the hot-set kernel's layout
     uint32_t *s_filter = s_q + NW * QCAP;
 
-    for (int i = threadIdx.x; i < a.n_sel; i += blockDim.x) s_fin[i] = a.fin[i];
+    fin_soa_store(s_fs, a.n_sel, a.fin);
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(a.filter);
         uint4 *dst = reinterpret_cast<uint4 *>(s_filter);
@@ -247,6 +359,7 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_pair(const K2Args a) {
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nsel = a.n_sel;
     const int half = lane >> 4, idx = lane & 15;
     const uint32_t hm = half ? 0xFFFF0000u : 0x0000FFFFu;
     const uint32_t lth = lanemask_lt() & hm;
@@ -281,11 +394,11 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_pair(const K2Args a) {
             if (PRE) {
                 if (cnt) comb = s.x;
             } else {
-                if (cnt) comb = __dadd_rn(0.0, fin_term(s_fin[s.meta & 0xFFFFu], s.x));
+                if (cnt) comb = __dadd_rn(0.0, fin_term_soa(s_fs, nsel, s.meta & 0xFFFFu, s.x));
 #pragma unroll 1
                 for (uint32_t i = 1; i < cnt; ++i) {
                     const Entry en = a.ovf[s.ovf + i - 1];
-                    comb = __dadd_rn(comb, fin_term(s_fin[en.j], en.x));
+                    comb = __dadd_rn(comb, fin_term_soa(s_fs, nsel, en.j, en.x));
                 }
             }
             v = clamp_ref(__dsub_rn(comb, occ_ret), occ_lim);
@@ -602,7 +715,7 @@ static size_t dense_coop_smem(int em_stride) {
 
 size_t k2_hotset_fixed_smem(int n_sel) {
     constexpr int NW = K2_THREADS / 32;
-    return (size_t)n_sel * sizeof(Fin) + (size_t)NW * 32 * sizeof(double) + (size_t)NW * QCAP * sizeof(uint32_t);
+    return (size_t)n_sel * sizeof(Fin) + (size_t)NW * VRING * sizeof(double) + (size_t)NW * QCAP * sizeof(uint32_t);
 }
 
 template <int HASH, bool CHECK, bool PRE>

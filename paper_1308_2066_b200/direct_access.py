@@ -80,7 +80,7 @@ class TableSet:
     """The direct-access tables of one layer / session, resident on the B200."""
 
     __slots__ = ("catalog_size", "tables", "fin_rate", "fin_ret", "fin_lim", "fin_share",
-                 "_dev", "_stacked", "_plans", "_lock", "__weakref__")
+                 "_dev", "_stacked", "_plans", "_lock", "_replicas", "__weakref__")
 
     def __init__(self, catalog_size: int, stacked, terms: Sequence[FinancialTerms],
                  nonzero: Sequence[int], *, _device_tables=None):
@@ -102,6 +102,7 @@ class TableSet:
         self.fin_share = np.array([t.share for t in terms], dtype=np.float64)
         self._plans: OrderedDict = OrderedDict()
         self._lock = threading.Lock()
+        self._replicas: dict[int, _native.Handle] = {}  # device -> copy of the tables (multi-GPU group)
         _count_build()
 
     @classmethod
@@ -176,11 +177,35 @@ class TableSet:
         return (sel, np.ascontiguousarray(self.fin_rate[sel]), np.ascontiguousarray(self.fin_ret[sel]),
                 np.ascontiguousarray(self.fin_lim[sel]), np.ascontiguousarray(self.fin_share[sel]))
 
-    def plan(self, rows, rate, ret, lim, share, pool: bool = False, precombine: bool = False) -> _native.Handle:
+    @property
+    def device(self) -> int:
+        """CUDA ordinal holding the tables."""
+        return _native.tables_device(self._dev)
+
+    def tables_on(self, device: int) -> _native.Handle:
+        """The tables in `device`'s memory: the original, or a peer copy made
+        once (the multi-GPU group replicates tables)."""
+        if device is None or device == self.device:
+            return self._dev
+        with self._lock:
+            rep = self._replicas.get(device)
+            if rep is None:
+                rep = self._replicas[device] = _native.tables_replicate(self._dev, device)
+            return rep
+
+    def plan(self, rows, rate, ret, lim, share, pool: bool = False, precombine: bool = False,
+             device: int | None = None) -> _native.Handle:
         """Device hot set for this selection + financial terms (cached, LRU);
         `pool` sizes it for the fused multi-layer kernel; `precombine` folds
-        the financial terms into one value per event."""
-        key = (pool, precombine, np.asarray(rows, np.int64).tobytes(),
+        the financial terms into one value per event (SURVEY 8(f) row 4);
+        `device` builds it on that GPU's replica of the tables.
+
+        An evicted plan is only dropped from the cache, never freed here: a
+        caller that still holds it (another thread's K2 launch, the
+        reference's concurrent run_trials, engine/__init__.py:195-200) keeps
+        it alive, and it is released when the last reference goes."""
+        dev = None if device is None or device == self.device else int(device)
+        key = (dev, pool, precombine, np.asarray(rows, np.int64).tobytes(),
                np.asarray(rate, np.float64).tobytes(), np.asarray(ret, np.float64).tobytes(),
                np.asarray(lim, np.float64).tobytes(), np.asarray(share, np.float64).tobytes())
         with self._lock:
@@ -188,12 +213,11 @@ class TableSet:
             if hit is not None:
                 self._plans.move_to_end(key)
                 return hit
-        plan = _native.plan_build(self._dev, rows, rate, ret, lim, share, pool=pool, precombine=precombine)
+        plan = _native.plan_build(self.tables_on(dev), rows, rate, ret, lim, share, pool=pool, precombine=precombine)
         with self._lock:
             self._plans[key] = plan
             while len(self._plans) > _PLAN_CACHE:
-                _, old = self._plans.popitem(last=False)
-                old.close()
+                self._plans.popitem(last=False)  # freed by its last holder (Handle.__del__)
         return plan
 
 

@@ -15,8 +15,10 @@ Backend naming: the reference accepts {"auto", "compiled", "python"}
 from __future__ import annotations
 
 import math
+import threading
 import time
 import weakref
+from collections import OrderedDict
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -151,6 +153,10 @@ _dense_cache: dict[int, tuple] = {}
 
 
 def _tables_for(stacked: np.ndarray):
+    if stacked.flags.writeable:
+        # the caller may change a writable array between calls (the reference
+        # kernel reads host memory every call): no device cache for it
+        return _DenseTables(stacked)
     key = id(stacked)
     hit = _dense_cache.get(key)
     if hit is not None and hit[0]() is stacked:
@@ -170,14 +176,22 @@ class _DenseTables:
     def __init__(self, stacked: np.ndarray):
         self.dev = _native.tables_from_dense(stacked)
         self.plans: dict = {}
+        self.lock = threading.Lock()
 
     def plan(self, rows, rate, ret, lim, share):
+        """Cached plan per (selection, terms).  The reference drives run_trials
+        from a thread pool (engine/__init__.py:195-200): an evicted plan is
+        only dropped from the cache; a thread still launching on it holds a
+        reference, and the plan is freed when the last one goes."""
         key = tuple(np.asarray(a).tobytes() for a in (rows, rate, ret, lim, share))
-        p = self.plans.get(key)
+        with self.lock:
+            p = self.plans.get(key)
         if p is None:
-            if len(self.plans) >= 8:
-                self.plans.pop(next(iter(self.plans))).close()
-            p = self.plans[key] = _native.plan_build(self.dev, rows, rate, ret, lim, share)
+            p = _native.plan_build(self.dev, rows, rate, ret, lim, share)
+            with self.lock:
+                p = self.plans.setdefault(key, p)
+                while len(self.plans) > 8:
+                    self.plans.pop(next(iter(self.plans)))
         return p
 
 
@@ -224,6 +238,16 @@ def run_trials(event_ids, offsets, stacked, rows, fin_rate, fin_ret, fin_lim, fi
 
 # -------------------------------------------------------------- the layer --
 
+def _group_devices(cfg: EngineConfig) -> tuple[int, ...]:
+    """GPUs a request runs on: worker_count > 1 spreads the reference's trial
+    ranges over up to worker_count GPUs (group.py); 1 = the current device."""
+    if cfg.worker_count <= 1:
+        return ()
+    from . import group
+
+    return group.devices_for(cfg.worker_count)
+
+
 def _simulate(yet, tset: TableSet, selection, terms: LayerTerms, cfg: EngineConfig, out: np.ndarray,
               validated: bool = False) -> int:
     """K2 over every trial of `yet` into `out`; `validated` = the ids were
@@ -232,6 +256,18 @@ def _simulate(yet, tset: TableSet, selection, terms: LayerTerms, cfg: EngineConf
     n = int(yet.offsets.shape[0]) - 1
     if n == 0:
         return 0
+    from . import group
+
+    if isinstance(yet, group.ShardedYearEventTable):  # HBM-resident on a GPU group
+        plans = group.plans_for(tset, yet.devices[: yet.n_shards], rows, rate, ret, lim, share, cfg.precombine)
+        return yet.run_layer(plans, terms, out, cfg.variant)
+    devices = _group_devices(cfg)
+    if len(devices) > 1 and getattr(yet, "_device", None) is None:
+        # worker_count > 1: the reference's trial ranges on a GPU group, one call
+        bounds = group.shard_bounds(np.asarray(yet.offsets), len(devices))
+        group.ensure_group(devices)
+        plans = group.plans_for(tset, devices[: bounds.size - 1], rows, rate, ret, lim, share, cfg.precombine)
+        return group.run_layer_host(yet, plans, bounds, terms, out, cfg.variant, validated)
     plan = tset.plan(rows, rate, ret, lim, share, precombine=cfg.precombine)
     resident = getattr(yet, "_device", None)
     if resident is not None:  # DeviceYearEventTable: ids already in HBM
@@ -297,15 +333,20 @@ def layer_pool(layers: Sequence[Layer]):
 
 
 _LAYER_TABLES: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_LAYER_TABLE_CACHE = 4  # pre-combined layer tables kept per pool plan (LRU)
 
 
 def _layer_table(plan, masks: np.ndarray, lt: np.ndarray, stream) -> _native.Handle:
     """Pre-combined occurrence table of one layer group (K1-L), cached per
     (pool plan, masks, layer terms)."""
-    per_plan = _LAYER_TABLES.setdefault(plan, {})
+    per_plan = _LAYER_TABLES.setdefault(plan, OrderedDict())
     key = (masks.tobytes(), lt.tobytes())
     hit = per_plan.get(key)
-    if hit is None:
+    if hit is not None:
+        per_plan.move_to_end(key)
+    else:
+        while len(per_plan) >= _LAYER_TABLE_CACHE:  # each table is 16 doubles per catalog event
+            per_plan.popitem(last=False)  # freed by its last holder
         h = _native._P()
         _native.check(_native.load().are_layer_table_build(
             plan.value, masks.shape[0], masks.ctypes.data, lt.ctypes.data, _native.ctypes.c_void_p(stream),
@@ -420,7 +461,10 @@ PROMOTE_CACHE = 2
 _promoted: dict[tuple, tuple] = {}  # (id(host YET), device) -> (weakref, DeviceYearEventTable)
 
 
-def _promote(yet):
+def _promote(yet, devices: tuple[int, ...] = ()):
+    """The HBM-resident copy of a large host YET (cached per host object):
+    a DeviceYearEventTable on the current GPU, or, for a GPU group
+    (worker_count > 1), a ShardedYearEventTable with one shard per GPU."""
     if getattr(yet, "_device", None) is not None or callable(getattr(yet, "yet_violations", None)):
         return yet
     n = int(yet.offsets[-1]) if yet.offsets.size else 0
@@ -428,7 +472,8 @@ def _promote(yet):
         return yet
     import torch
 
-    key = (id(yet), torch.cuda.current_device())  # a copy serves the device it lives on
+    # a copy serves the device(s) it lives on
+    key = (id(yet), devices if len(devices) > 1 else torch.cuda.current_device())
     hit = _promoted.get(key)
     if hit is not None and hit[0]() is yet:
         _promoted[key] = _promoted.pop(key)  # most recent last
@@ -436,10 +481,15 @@ def _promote(yet):
 
     from .resident import DeviceYearEventTable
 
-    free, _ = torch.cuda.mem_get_info()
-    if 4 * n + 8 * int(yet.offsets.size) > free // 2:  # leave room for tables and outputs
-        return yet
-    dyet = DeviceYearEventTable(yet)
+    if len(devices) > 1:
+        from .group import ShardedYearEventTable
+
+        dyet = ShardedYearEventTable(yet, devices)
+    else:
+        free, _ = torch.cuda.mem_get_info()
+        if 4 * n + 8 * int(yet.offsets.size) > free // 2:  # leave room for tables and outputs
+            return yet
+        dyet = DeviceYearEventTable(yet)
     try:
         ref = weakref.ref(yet, lambda _r, k=key: _promoted.pop(k, None))
     except TypeError:  # not weak-referenceable: no caching
@@ -455,13 +505,17 @@ def run_aggregate_analysis_with_stats(layers: Sequence[Layer], yet, cfg: EngineC
                                       pool=None) -> tuple[list[YearLossTable], RunStats]:
     """Validate, then per layer: K1 build (build_seconds), K2 (sim_seconds)."""
     cfg = cfg or EngineConfig()
-    yet = _promote(yet)
+    devices = _group_devices(cfg)
+    yet = _promote(yet, devices)
     violations = validate_portfolio(layers, yet)
     if violations:
         raise PortfolioInvalidError(violations)
     stats = RunStats(trials=int(yet.offsets.shape[0]) - 1, layers=len(layers))
     ylts: list[YearLossTable] = []
-    fused = _fusable(layers, cfg, int(yet.catalog_size), int(yet.offsets[-1]) if yet.offsets.size else 0)
+    # the fused multi-layer kernel runs on one GPU; a GPU group runs the
+    # layers one by one, each over every GPU
+    fused = None if len(devices) > 1 else _fusable(layers, cfg, int(yet.catalog_size),
+                                                   int(yet.offsets[-1]) if yet.offsets.size else 0)
     if fused is not None and stats.trials > 0:
         # one pass over the YET for every layer (SURVEY.md §8(f) row 2)
         from .resident import DeviceYearEventTable
@@ -472,8 +526,11 @@ def run_aggregate_analysis_with_stats(layers: Sequence[Layer], yet, cfg: EngineC
         tset = TableSet.from_elts(pool, yet.catalog_size)
         tset.plan(*tset.selection_arrays(None), pool=True)
         stats.build_seconds += time.perf_counter() - t0
-        stats.peak_table_bytes = memory_footprint(tset.tables).total_bytes
-        dyet = yet if getattr(yet, "_device", None) is not None else DeviceYearEventTable(yet)
+        # the reference reports the largest per-layer footprint (engine/__init__.py:244-247)
+        stats.peak_table_bytes = memory_footprint(tset.tables[:max(len(la.elts) for la in layers)]).total_bytes
+        # validate_portfolio has checked the host YET already: upload ids + offsets only
+        dyet = yet if getattr(yet, "_device", None) is not None else DeviceYearEventTable.from_host_arrays(
+            yet.catalog_size, yet.event_ids, yet.offsets)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         d = simulate_layers_device(dyet, tset, masks, [layer.terms for layer in layers], precombine=cfg.precombine)

@@ -277,3 +277,23 @@ def test_validation_report_equals_reference_fixture():
         layers, yet = build(case)
         got = [str(v) for v in validate_portfolio(layers, yet)]
         assert got == case["report"], case["name"]
+
+
+def test_group_shard_bounds_follow_the_reference_partition(golden):
+    """The trial -> GPU cut points are split_by_events (engine/__init__.py:151-159)."""
+    from paper_1308_2066_b200.group import shard_bounds
+
+    for case in golden["split_by_events"]:
+        offs = np.zeros(len(case["lens"]) + 1, np.int64)
+        np.cumsum(case["lens"], out=offs[1:])
+        b = shard_bounds(offs, case["parts"])
+        assert b[0] == 0 and b[-1] == len(case["lens"]) and np.all(np.diff(b) > 0)
+        assert [[int(x), int(y)] for x, y in zip(b[:-1], b[1:])] == case["batches"]
+
+
+def test_group_devices_env(monkeypatch):
+    from paper_1308_2066_b200 import group
+
+    monkeypatch.setenv("ARE_GROUP_DEVICES", "0,0,1")
+    assert group.devices_for(8) == (0, 0, 1)
+    assert group.devices_for(2) == (0, 0)
