@@ -90,6 +90,8 @@ struct Workspace {
     double *d_out = nullptr;
     int64_t cap_out = 0;
     unsigned int *d_err = nullptr;
+    double *d_k3 = nullptr;  // are_order_stats_host's device copy of the YLT
+    int64_t cap_k3 = 0;
 };
 static Workspace g_ws[64];
 static constexpr int64_t CHUNK_OCC = 32ll << 20;  // 32 Mi occurrences (128 MiB of ids) per chunk
@@ -906,20 +908,21 @@ int are_order_stats_host(const double *losses, int64_t n, const double *rps, int
     if ((rc = current_device(&dev))) return rc;
     DeviceInfo *di;
     if ((rc = use_device(dev, &di))) return rc;
-    cudaStream_t st;
-    ARE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    double *d = nullptr;
-    cudaError_t e = cudaMallocAsync(&d, n * sizeof(double), st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d, losses, n * sizeof(double), cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) {
-        cudaStreamDestroy(st);
-        return cuda_fail(e, "upload year loss table");
+    // the device's cached workspace: its stream and a YLT buffer kept across
+    // calls (no stream or allocation churn on the per-request path; creating
+    // and destroying them per call stalled for 0.1-0.8 s on the bench boxes)
+    Workspace &w = g_ws[dev];
+    std::lock_guard<std::mutex> guard(w.mu);
+    if ((rc = ws_reserve(w, 0, 0, 0, false))) return rc;
+    if (n > w.cap_k3) {
+        cudaFree(w.d_k3);
+        w.d_k3 = nullptr;
+        w.cap_k3 = 0;
+        ARE_CUDA(cudaMalloc(&w.d_k3, n * sizeof(double)));
+        w.cap_k3 = n;
     }
-    rc = k3_order_stats(d, n, rps, n_rp, pml_out, tvar_out, di->sms, st);
-    cudaFreeAsync(d, st);
-    cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
-    return rc;
+    ARE_CUDA(cudaMemcpyAsync(w.d_k3, losses, n * sizeof(double), cudaMemcpyHostToDevice, w.comp));
+    return k3_order_stats(w.d_k3, n, rps, n_rp, pml_out, tvar_out, di->sms, w.comp);
 }
 
 int are_rollup_device(const double *const *d_ylts, int64_t n_layers, int64_t n, double *d_out, void *stream) {

@@ -126,9 +126,13 @@ def test_every_visible_gpu():
     want, _ = run_aggregate_analysis_with_stats(layers, yet, EngineConfig(worker_count=1))
     got, _ = run_aggregate_analysis_with_stats(layers, yet, EngineConfig(worker_count=max(n, 2)))
     assert [y.losses.tobytes() for y in got] == [y.losses.tobytes() for y in want]
-    size = _native._I32()
-    _native.check(_native.load().are_group_size(ctypes.byref(size)))
-    assert size.value == n
+    from paper_1308_2066_b200.group import devices_for
+
+    assert devices_for(max(n, 2)) == tuple(range(n))
+    if n > 1:
+        size = _native._I32()
+        _native.check(_native.load().are_group_size(ctypes.byref(size)))
+        assert size.value == n
 
 
 def test_group_calls_keep_the_callers_device():
