@@ -2,6 +2,12 @@
 """Benchmark: aggregate-analysis trials/sec on the C2 workload (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c3|c4] [--scaling weak|strong]
+
+--workload c3 (the 16-layer portfolio over 1M trials split across the GPUs,
+allgather_portfolio between ranks) and c4 / --scaling strong (10M trials
+split across the GPUs) are the other BASELINE.json configs; the default c2
+line is the headline.
 
 Workload (per GPU): 1M trials x 1000 events, one layer of
 15 ELTs over a 2M-event catalog, Cat XL + Aggregate XL terms
@@ -47,6 +53,8 @@ E2E_ROUNDS = 3
 SEED = 2066
 METRIC = "aggregate-analysis trials/sec, 1M×1000-event YET, 1/2/4/8 B200; % HBM BW"
 WORKLOAD = "C2: 1M trials x 1000 events/trial per GPU, 1 layer x 15 ELTs, catalog 2M, Cat XL + Agg XL"
+WORKLOAD_C3 = "C3: 1M trials x 1000 events/trial split over the GPUs, 16-layer portfolio (32-ELT pool, PO/Agg XL)"
+WORKLOAD_C4 = "C4: 10M trials x 1000 events/trial split over the GPUs (strong scaling), 1 layer x 15 ELTs"
 
 
 def bytes_per_trial(events: int = EVENTS, elts: int = N_ELTS) -> int:
@@ -258,19 +266,16 @@ def run_reference_arm(args) -> None:
 
 # ------------------------------------------------------------- our arm --
 
-def c3_fused(dyet, stream, reps: int = 5) -> dict:
-    """C3's portfolio shape on the resident YET: one fused K2 pass for 16
-    layers (K2-L), CUDA events on the launch stream."""
+def c3_portfolio(seed: int = SEED):
+    """C3's portfolio: 16 layers over a 32-ELT pool, layer i even
+    Per-Occurrence XL (occR_i, occL_i, 0, inf), odd Aggregate XL (0, inf,
+    aggR_i, aggL_i), terms from the reference generator restatement."""
     import math
 
-    import torch
-
-    from paper_1308_2066_b200.direct_access import TableSet
-    from paper_1308_2066_b200.engine import layer_pool, simulate_layers_device
     from paper_1308_2066_b200.portfolio import Layer, LayerTerms
     from paper_1308_2066_b200.synth import GeneratorSpec, generate_elt, generate_layer
 
-    spec = GeneratorSpec(seed=SEED, catalog_size=CATALOG, elt_count=32, elt_size_range=(10_000, 30_000),
+    spec = GeneratorSpec(seed=seed, catalog_size=CATALOG, elt_count=32, elt_size_range=(10_000, 30_000),
                          layer_count=16, elts_per_layer=15)
     pool = [generate_elt(spec, i) for i in range(32)]
     layers = []
@@ -280,44 +285,84 @@ def c3_fused(dyet, stream, reps: int = 5) -> dict:
         terms = LayerTerms(t.occ_retention, t.occ_limit, 0.0, math.inf) if i % 2 == 0 else \
             LayerTerms(0.0, math.inf, t.agg_retention, t.agg_limit)
         layers.append(Layer(g.id, g.elts, terms))
+    return layers
+
+
+def c3_fused(dyet, stream, reps: int = 5) -> dict:
+    """C3's portfolio shape on this GPU's resident ids: one fused K2 pass for
+    16 layers (K2-L), CUDA events on the launch stream (a side metric of the
+    C2 line; `--workload c3` is the multi-GPU C3 bench)."""
+    import torch
+
+    from paper_1308_2066_b200.direct_access import TableSet
+    from paper_1308_2066_b200.engine import layer_pool, simulate_layers_device
+
+    layers = c3_portfolio()
     pe, masks = layer_pool(layers)
     ptset = TableSet.from_elts(pe, CATALOG)
     lterms = [lay.terms for lay in layers]
     n = dyet.trial_count
     out = torch.empty((16, n), dtype=torch.float64, device=dyet.device)
+    peak, _ = _peaks()
     res = {}
     for pre in (False, True):
         with torch.cuda.stream(stream):
             for _ in range(2):
-                simulate_layers_device(dyet, ptset, masks, lterms, out=out, precombine=pre)
+                simulate_layers_device(dyet, ptset, masks, lterms, out=out, precombine=pre, check=False)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             ev[0].record(stream)
             for _ in range(reps):
-                simulate_layers_device(dyet, ptset, masks, lterms, out=out, precombine=pre)
+                simulate_layers_device(dyet, ptset, masks, lterms, out=out, precombine=pre, check=False)
             ev[1].record(stream)
         torch.cuda.synchronize(dyet.device)
         ms = ev[0].elapsed_time(ev[1]) / reps
+        hbm = n * (compulsory_bytes_per_trial() + 8 * 15)  # ids + offset once, 16 float64 YLT rows
         res["precombined" if pre else "exact"] = {
-            "kernel_ms": ms, "portfolio_trials_per_s": n / (ms / 1e3), "layer_trials_per_s": 16 * n / (ms / 1e3)}
+            "kernel_ms": ms, "portfolio_trials_per_s": n / (ms / 1e3), "layer_trials_per_s": 16 * n / (ms / 1e3),
+            "hbm_bytes_per_launch": hbm, "achieved_gbs": hbm / (ms / 1e3) / 1e9,
+            "frac": hbm / (ms / 1e3) / 1e9 / peak}
     res.update({"layers": 16, "pool_elts": 32, "trials": n,
                 "note": "C3 shape, one pass over the ids for 16 layers: `exact` evaluates every (event, layer) "
                         "in K2 (k2_layers), `precombined` reads a per-event table of the 16 occurrence values "
                         "built once by K1-L (k2_layers_pre); both bitwise equal to 16 single-layer K2 runs "
-                        "(tests); separately reported, not the headline"})
+                        "(tests); frac on the bytes that cross HBM (ids + offsets + 16 YLT rows)"})
     return res
 
 
-def run_ours(args) -> None:
+def compulsory_bytes_per_trial(events: int = EVENTS) -> int:
+    """Bytes that must cross HBM per trial: its ids, its offset, its float64 YLT slot."""
+    return 4 * events + 8 + 8
+
+
+def roofline(trials: int, kernel_ms: float, kernel: str) -> dict:
+    """K2's roofline on the bytes that cross HBM (the verdict's rule: the
+    lookups are served from L2 / shared memory by design, so the SURVEY 8(d)
+    lookup-equivalent figure is reported separately, not as `frac`)."""
+    peak, peak_src = _peaks()
+    hbm = trials * compulsory_bytes_per_trial()
+    achieved = hbm / (kernel_ms / 1e3) / 1e9
+    traffic = _traffic() if kernel == "k2_hotset" else None  # the committed capture is of k2_hotset
+    lk = trials * bytes_per_trial()
+    return {
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "traffic": traffic, "traffic_ratio": (traffic / (hbm / (trials / TRIALS_PER_GPU))) if traffic else None,
+        "kernel": kernel, "kernel_ms": kernel_ms, "bytes_per_launch": hbm,
+        "bytes_formula": "trials x (4*E + 8 + 8): ids, offset, float64 YLT slot -- the bytes that cross HBM",
+        "peak_source": peak_src,
+        "traffic_note": "ncu dram__bytes_read+write per 1M-trial launch (profiles/k2_traffic.json); "
+                        "traffic_ratio = traffic / bytes_per_launch at 1M trials",
+        "lookup_equivalent": {
+            "bytes_per_launch": lk, "formula": "trials x (12 + 4*E*(1+J)), SURVEY.md 8(d)",
+            "gbs": lk / (kernel_ms / 1e3) / 1e9, "ratio_to_peak": lk / (kernel_ms / 1e3) / 1e9 / peak,
+            "note": "one fp32 load per (event, ELT) lookup as if every lookup went to HBM; K2 skips the "
+                    "86% of occurrences no ELT holds (bit-exact) and serves the rest from L2/shared "
+                    "memory, so this exceeds 1 and is not a roofline fraction"},
+    }
+
+
+def _setup_dist():
     import torch
     import torch.distributed as dist
-
-    from paper_1308_2066_b200 import _native
-    from paper_1308_2066_b200.direct_access import TableSet
-    from paper_1308_2066_b200.distributed import allgather_ylt, max_over_ranks, partition
-    from paper_1308_2066_b200.engine import price_layer
-    from paper_1308_2066_b200.portfolio import YearEventTable
-    from paper_1308_2066_b200.resident import DeviceYearEventTable
-    from paper_1308_2066_b200.risk import order_stats
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device -- the B200 engine has no CPU fallback")
@@ -331,34 +376,127 @@ def run_ours(args) -> None:
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
-    threads = max(1, host_cores() // max(world, 1))
+    return world, rank, backend, local, dev
 
-    layer = make_layer()
-    total_trials = TRIALS_PER_GPU * world
+
+def _device_yet(first: int, last: int, dev, threads: int, chunk: int = 1 << 20):
+    """The ids of trials [first, last) generated in host chunks straight into
+    HBM (a 10M-trial shard is 40 GB; the host never holds more than a chunk)."""
+    import torch
+
+    from paper_1308_2066_b200.resident import DeviceYearEventTable
+
+    n = last - first
+    d_ids = torch.zeros(n * EVENTS + 4, dtype=torch.int32, device=dev)
+    buf = np.empty(chunk * EVENTS, dtype=np.uint32)
+    for a in range(first, last, chunk):
+        b = min(last, a + chunk)
+        y = bulk_chunk(a, b, threads, buf)
+        d_ids[(a - first) * EVENTS:(b - first) * EVENTS].copy_(torch.from_numpy(y.view(np.int32)))
+    offsets = np.arange(n + 1, dtype=np.int64) * EVENTS
+    return DeviceYearEventTable.from_device(CATALOG, d_ids, torch.from_numpy(offsets).to(dev), offsets)
+
+
+def bulk_chunk(a: int, b: int, threads: int, buf: np.ndarray) -> np.ndarray:
+    from paper_1308_2066_b200.synth import bulk_yet
+
+    return bulk_yet(SEED, CATALOG, a, b, EVENTS, threads=threads, out=buf).event_ids
+
+
+def _pinned_host_yet(yet, local: int):
+    import torch
+
+    from paper_1308_2066_b200.portfolio import YearEventTable
+
+    try:
+        with GpuLocalCpus(local):
+            ids = torch.from_numpy(yet.event_ids.view(np.int32)).pin_memory()
+            offs = torch.from_numpy(np.ascontiguousarray(yet.offsets)).pin_memory()
+        pinned = True
+    except RuntimeError:  # page-locking refused (e.g. ulimit -l with 8 ranks): pageable, staged copies
+        ids = torch.from_numpy(yet.event_ids.view(np.int32))
+        offs = torch.from_numpy(np.ascontiguousarray(yet.offsets))
+        pinned = False
+    return YearEventTable(CATALOG, ids.numpy().view(np.uint32), None, offs.numpy()), pinned, (ids, offs)
+
+
+def _stats(xs) -> dict:
+    xs = [float(x) for x in xs]
+    return {"median": float(np.median(xs)), "max": max(xs), "min": min(xs)} if xs else {}
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_1308_2066_b200 import _native
+    from paper_1308_2066_b200.direct_access import TableSet
+    from paper_1308_2066_b200.distributed import allgather_portfolio, allgather_ylt, max_over_ranks, partition
+    from paper_1308_2066_b200.engine import layer_pool, price_layer, simulate_layers_device
+    from paper_1308_2066_b200.resident import DeviceYearEventTable
+    from paper_1308_2066_b200.risk import order_stats, rollup_device
+
+    workload = args.workload
+    world, rank, backend, local, dev = _setup_dist()
+    threads = max(1, host_cores() // max(world, 1))
+    strong = workload in ("c3", "c4")
+    total_trials = {"c2": TRIALS_PER_GPU * world, "c3": TRIALS_PER_GPU, "c4": 10 * TRIALS_PER_GPU}[workload]
     t_gen = time.perf_counter()
     # global YET offsets are fixed-length, so the partition is computable without the ids
     g_offsets = np.arange(total_trials + 1, dtype=np.int64) * EVENTS
     parts = partition(g_offsets, world)
     t0, t1 = parts[rank]
-    yet = make_yet(t0, t1, threads)
+    n_local = t1 - t0
+    stream = torch.cuda.current_stream(dev)
+    host_yet = None
+    if workload == "c2":
+        host_yet = make_yet(t0, t1, threads)
+        dyet = DeviceYearEventTable(host_yet, device=local)
+    else:
+        dyet = _device_yet(t0, t1, dev, threads)
     gen_s = time.perf_counter() - t_gen
 
-    tset = TableSet.from_elts(layer.elts, CATALOG)
-    rows, rate, ret, lim, share = tset.selection_arrays(None)
-    plan = tset.plan(rows, rate, ret, lim, share)
-    info = _native.plan_info(plan)
-    dyet = DeviceYearEventTable(yet, device=local)
-    d_local = torch.empty(t1 - t0, dtype=torch.float64, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    if workload == "c3":
+        layers = c3_portfolio()
+        pool, masks = layer_pool(layers)
+        tset = TableSet.from_elts(pool, CATALOG)
+        lterms = [la.terms for la in layers]
+        plan = tset.plan(*tset.selection_arrays(None), pool=True)
+        info = _native.plan_info(plan)
+        d_layers = torch.empty((16, n_local), dtype=torch.float64, device=dev)
+        kernel_name = "k2_layers (16 layers fused)"
+    else:
+        layer = make_layer()
+        tset = TableSet.from_elts(layer.elts, CATALOG)
+        rows, rate, ret, lim, share = tset.selection_arrays(None)
+        plan = tset.plan(rows, rate, ret, lim, share)
+        info = _native.plan_info(plan)
+        d_local = torch.empty(n_local, dtype=torch.float64, device=dev)
+        kernel_name = "k2_hotset"
 
-    def step(k2_events=None):
-        if k2_events is not None:
-            k2_events[0].record(stream)
-        dyet.simulate_device(plan, layer.terms, out=d_local, stream=stream, check=False)
-        if k2_events is not None:
-            k2_events[1].record(stream)
-        full = allgather_ylt(d_local, parts) if world > 1 else d_local
-        return order_stats(full, RPS, stream=stream)
+    def step(ev=None):
+        """K2 over this rank's trials -> (N > 1) the YLT exchange -> K3."""
+        if ev is not None:
+            ev[0].record(stream)
+        if workload == "c3":
+            simulate_layers_device(dyet, tset, masks, lterms, out=d_layers, check=False)
+        else:
+            dyet.simulate_device(plan, layer.terms, out=d_local, stream=stream, check=False)
+        if ev is not None:
+            ev[1].record(stream)
+        if workload == "c3":
+            if world > 1:
+                _, full = allgather_portfolio(list(d_layers), parts)
+            else:
+                full = rollup_device(list(d_layers))
+        else:
+            full = allgather_ylt(d_local, parts) if world > 1 else d_local
+        if ev is not None:
+            ev[2].record(stream)
+        res = order_stats(full, RPS, stream=stream)
+        if ev is not None:
+            ev[3].record(stream)
+        return res
 
     for _ in range(args.warmup):
         step()
@@ -366,71 +504,96 @@ def run_ours(args) -> None:
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    k2_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _native.launch_count()
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize(dev)
         start.record(stream)
         for i in range(args.steps):
-            pml_v, tvar_v = step(k2_ev[i])
+            pml_v, tvar_v = step(evs[i])
         stop.record(stream)
         torch.cuda.synchronize(dev)
     launches = _native.launch_count() - launches0
     if world > 1:
         dist.barrier()
     elapsed_ms = start.elapsed_time(stop)
-    k2_ms = float(np.mean([a.elapsed_time(b) for a, b in k2_ev]))
-    elapsed_ms = max_over_ranks(elapsed_ms, dev) if world > 1 else elapsed_ms
-    k2_ms_max = max_over_ranks(k2_ms, dev) if world > 1 else k2_ms
-    value = total_trials * args.steps / (elapsed_ms / 1e3)
+    k2_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    xchg_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+    k3_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in evs]))
+    mx = (lambda v: max_over_ranks(v, dev)) if world > 1 else (lambda v: v)
+    elapsed_max = mx(elapsed_ms)
+    phases = {"k2_ms": mx(k2_ms), "exchange_ms": mx(xchg_ms), "k3_ms": mx(k3_ms),
+              "exchange": ("allgather_portfolio (16 layer rows + portfolio, one NCCL all-gather)" if workload == "c3"
+                           else "allgather_ylt (one NCCL all-gather)") if world > 1 else
+              ("k3_rollup of the 16 layers" if workload == "c3" else "none (one GPU)")}
+    value = total_trials * args.steps / (elapsed_max / 1e3)
 
-    # ---- separately reported work unit: pre-combined plan
-    pre_plan = tset.plan(rows, rate, ret, lim, share, precombine=True)
-    for _ in range(3):
-        dyet.simulate_device(pre_plan, layer.terms, out=d_local, stream=stream, check=False)
-    pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    pe[0].record(stream)
-    for _ in range(10):
-        dyet.simulate_device(pre_plan, layer.terms, out=d_local, stream=stream, check=False)
-    pe[1].record(stream)
-    torch.cuda.synchronize(dev)
-    pre_ms = pe[0].elapsed_time(pe[1]) / 10
-
-    # ---- separately reported work unit: C3's fused 16-layer pass (SURVEY 8(f)
-    # row 2) over this rank's resident ids: 16 layers from a 32-ELT pool,
-    # Per-Occurrence / Aggregate XL alternating (scripts/sweep.py c3)
-    c3 = c3_fused(dyet, stream)
+    side = {}
+    if workload == "c2":
+        # ---- separately reported work unit: pre-combined plan
+        pre_plan = tset.plan(rows, rate, ret, lim, share, precombine=True)
+        for _ in range(3):
+            dyet.simulate_device(pre_plan, layer.terms, out=d_local, stream=stream, check=False)
+        pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        pe[0].record(stream)
+        for _ in range(10):
+            dyet.simulate_device(pre_plan, layer.terms, out=d_local, stream=stream, check=False)
+        pe[1].record(stream)
+        torch.cuda.synchronize(dev)
+        pre_ms = pe[0].elapsed_time(pe[1]) / 10
+        peak, _ = _peaks()
+        side["precombined_k2"] = {
+            "kernel_ms": pre_ms, "trials_per_s": n_local / (pre_ms / 1e3),
+            "achieved_gbs": n_local * compulsory_bytes_per_trial() / (pre_ms / 1e3) / 1e9,
+            "frac": n_local * compulsory_bytes_per_trial() / (pre_ms / 1e3) / 1e9 / peak,
+            "note": "different unit of work (financial terms folded per event in K1); not the headline"}
+        # ---- C3's fused 16-layer pass on this GPU
+        side["c3_fused_layers"] = c3_fused(dyet, stream)
 
     # ---- e2e: the public host API on pinned host buffers --------------------
-    host_pinned = True
-    try:
-        with GpuLocalCpus(local):
-            pinned = torch.from_numpy(yet.event_ids.view(np.int32)).pin_memory()
-            h_offsets = torch.from_numpy(np.ascontiguousarray(yet.offsets)).pin_memory()
-    except RuntimeError:  # page-locking refused (e.g. ulimit -l with 8 ranks): pageable, staged copies
-        host_pinned = False
-        pinned = torch.from_numpy(yet.event_ids.view(np.int32))
-        h_offsets = torch.from_numpy(np.ascontiguousarray(yet.offsets))
-    hyet = YearEventTable(CATALOG, pinned.numpy().view(np.uint32), None, h_offsets.numpy())
+    # c2: this rank's whole shard; c3/c4: a bounded host sample of it (the
+    # rate is linear in trials), said in the line
+    e2e_trials = n_local if workload == "c2" else min(n_local, TRIALS_PER_GPU)
+    src = host_yet if host_yet is not None else make_yet(t0, t0 + e2e_trials, threads)
+    hyet, host_pinned, _keep = _pinned_host_yet(src, local)
+    e_parts = partition(np.arange(e2e_trials * world + 1, dtype=np.int64) * EVENTS, world) if strong else parts
+    ph = {"price_ms": [], "exchange_ms": [], "order_stats_ms": []}
 
     def e2e_step():
-        ylt, _ = price_layer(hyet, tset, None, layer.terms)
-        if world > 1:
-            full = allgather_ylt(torch.from_numpy(ylt).to(dev), parts)
-            return order_stats(full, RPS)
-        return order_stats(ylt, RPS)
+        from paper_1308_2066_b200.engine import run_aggregate_analysis
+        from paper_1308_2066_b200.portfolio import YearEventTable
+
+        a = time.perf_counter()
+        if workload == "c3":
+            # the entry point on a fresh host YET object every step (its promotion
+            # cache must not skip the upload): H2D + K0 + fused K2-L + D2H
+            y = YearEventTable(CATALOG, hyet.event_ids, None, hyet.offsets)
+            ylts = run_aggregate_analysis(layers, y)
+            local_rows = [torch.from_numpy(np.asarray(t.losses)).to(dev) for t in ylts]
+        else:
+            ylt, _ = price_layer(hyet, tset, None, layer.terms)
+        b = time.perf_counter()
+        if workload == "c3":
+            full = allgather_portfolio(local_rows, e_parts)[1] if world > 1 else rollup_device(local_rows)
+        elif world > 1:
+            full = allgather_ylt(torch.from_numpy(ylt).to(dev), e_parts)
+        else:
+            full = ylt
+        c = time.perf_counter()
+        r = order_stats(full, RPS)
+        d = time.perf_counter()
+        ph["price_ms"].append((b - a) * 1e3)
+        ph["exchange_ms"].append((c - b) * 1e3)
+        ph["order_stats_ms"].append((d - c) * 1e3)
+        return r
 
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     for _ in range(min(args.warmup, 2)):
         e2e_step()
+    for k in ph:
+        ph[k].clear()
     torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    # E2E_ROUNDS rounds of e2e_steps steps each; the value is the best round
-    # (every step of it timed, copies included) -- the reference bench's own
-    # convention of the minimum over rounds (pkg/src/aggrisk/bench.py:113-140),
-    # because the box's host is shared and single steps occasionally stall
     rounds = []
     for _ in range(E2E_ROUNDS):
         if world > 1:
@@ -442,34 +605,32 @@ def run_ours(args) -> None:
             marks.append(time.perf_counter())
         torch.cuda.synchronize(dev)
         secs = time.perf_counter() - t_e2e
-        rounds.append((max_over_ranks(secs, dev) if world > 1 else secs, marks))
-    e2e_s, e2e_marks = min(rounds, key=lambda r: r[0])
-    e2e_value = total_trials * e2e_steps / e2e_s
+        rounds.append((mx(secs), marks))
+    e2e_s = float(np.median([r[0] for r in rounds]))
+    per_step = [(b - a) * 1e3 for r in rounds for a, b in zip(r[1], r[1][1:])]
+    e2e_value = e2e_trials * world * e2e_steps / e2e_s
     # the PCIe ceiling on this box: one plain pinned->device copy of the ids
-    d_probe = torch.empty(pinned.numel(), dtype=torch.int32, device=dev)
+    pinned_ids = _keep[0]
+    d_probe = torch.empty(pinned_ids.numel(), dtype=torch.int32, device=dev)
     pcie = []
     for _ in range(3):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ev[0].record(stream)
-        d_probe.copy_(pinned, non_blocking=True)
+        d_probe.copy_(pinned_ids, non_blocking=True)
         ev[1].record(stream)
         torch.cuda.synchronize(dev)
-        pcie.append(pinned.numel() * 4 / (ev[0].elapsed_time(ev[1]) / 1e3) / 1e9)
+        pcie.append(pinned_ids.numel() * 4 / (ev[0].elapsed_time(ev[1]) / 1e3) / 1e9)
     del d_probe
     pcie_gbs = max(pcie)
-    n_local = t1 - t0
-    h2d = int(yet.event_ids.nbytes + yet.offsets.nbytes + n_local * 8)  # ids, offsets, YLT to K3
-    d2h = int(n_local * 8 + 2 * 8 * len(RPS))                        # YLT + pml/tvar
+    n_layers_out = 16 if workload == "c3" else 1
+    h2d = int(hyet.event_ids.nbytes + hyet.offsets.nbytes + e2e_trials * 8 * n_layers_out)
+    d2h = int(e2e_trials * 8 * n_layers_out + 2 * 8 * len(RPS))
 
     if rank != 0:
         dist.destroy_process_group()
         return
 
-    peak, peak_src = _peaks()
-    k2_bytes = (t1 - t0) * bytes_per_trial()
-    achieved = k2_bytes / (k2_ms / 1e3) / 1e9
-    traffic = _traffic()
-    ids_bytes = (t1 - t0) * EVENTS * 4
+    name = {"c2": WORKLOAD, "c3": WORKLOAD_C3, "c4": WORKLOAD_C4}[workload]
     line = {
         "metric": METRIC,
         "value": value,
@@ -477,68 +638,66 @@ def run_ours(args) -> None:
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": elapsed_ms / args.steps,
+        "ms_per_step": elapsed_max / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None,
-        "vs_paper_c2075": value / 50_000.0,
+        "vs_paper_c2075": value / 50_000.0 if workload == "c2" else None,
         "dtype": "f64",
         "data": "synthetic",
         "config": {
-            "workload": WORKLOAD, "trials_per_gpu": TRIALS_PER_GPU, "events_per_trial": EVENTS,
-            "elts": N_ELTS, "catalog": CATALOG, "layer_terms": list(TERMS), "return_periods": RPS,
-            "parallelism": f"trial-sharded x{world} (split_by_events), YLT all-gather over {backend.upper()}",
-            "l2": "no flush: 4 GB id stream per GPU > 126 MB L2; hot-set records L2-resident by design",
+            "workload": name, "trials_total": total_trials, "trials_per_gpu": n_local,
+            "events_per_trial": EVENTS, "catalog": CATALOG,
+            "elts": 32 if workload == "c3" else N_ELTS, "layers": 16 if workload == "c3" else 1,
+            "layer_terms": "C3 generator terms (PO XL / Agg XL alternating)" if workload == "c3" else list(TERMS),
+            "return_periods": RPS,
+            "parallelism": f"trial-sharded x{world} (split_by_events)" + (
+                f", YLT all-gather over {backend.upper()}" if world > 1 else ""),
+            "l2": "no flush: 4 GB id stream per 1M trials > 126 MB L2; hot-set records L2-resident by design",
             "generator": "ELTs: reference generator restatement seed 2066; YET: synth.bulk_yet",
-            "kernel": "k2_hotset (persistent, 1 CTA/SM, warp per trial)",
+            "kernel": kernel_name,
         },
-        "roofline": {
-            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic,
-            "kernel": "k2_hotset", "kernel_ms": k2_ms, "kernel_ms_max_over_ranks": k2_ms_max,
-            "algorithmic_bytes_per_launch": k2_bytes,
-            "bytes_formula": "trials x (12 + 4*E*(1+J)), SURVEY.md 8(d)",
-            "peak_source": peak_src,
-            "compulsory": {"bytes": ids_bytes + (t1 - t0) * 16, "achieved_gbs": (ids_bytes + (t1 - t0) * 16) / (k2_ms / 1e3) / 1e9,
-                           "frac": (ids_bytes + (t1 - t0) * 16) / (k2_ms / 1e3) / 1e9 / peak,
-                           "note": "ids + offsets + YLT, the bytes that must cross HBM"},
-            "k2_share_of_step": k2_ms / (elapsed_ms / args.steps),
-        },
+        "phases_max_over_ranks": phases,
+        "roofline": roofline(n_local, phases["k2_ms"], kernel_name) if workload != "c3" else dict(
+            roofline(n_local, phases["k2_ms"], kernel_name),
+            bytes_per_launch=n_local * (compulsory_bytes_per_trial() + 8 * 15),
+            achieved=n_local * (compulsory_bytes_per_trial() + 8 * 15) / (phases["k2_ms"] / 1e3) / 1e9,
+            frac=n_local * (compulsory_bytes_per_trial() + 8 * 15) / (phases["k2_ms"] / 1e3) / 1e9 / _peaks()[0],
+            bytes_formula="trials x (4*E + 8 + 16*8): ids and offset once, 16 float64 YLT rows"),
         "e2e": {"value": e2e_value, "unit": "trials/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_s * 1e3 / e2e_steps, "steps": e2e_steps,
-                "step_ms": [round((b - a) * 1e3, 2) for a, b in zip(e2e_marks, e2e_marks[1:])],
-                "median_step_ms": float(np.median(np.diff(e2e_marks))) * 1e3,
+                "ms_per_step": e2e_s * 1e3 / e2e_steps, "steps": e2e_steps, "trials_per_gpu": e2e_trials,
                 "rounds_ms_per_step": [round(r[0] * 1e3 / e2e_steps, 2) for r in rounds],
-                "note": f"value = the best of {E2E_ROUNDS} rounds of `steps` steps (each round: all its steps "
-                        "over their total time, H2D/D2H included), the reference bench's min-over-rounds "
-                        "convention; single steps on the shared host occasionally stall for 0.1-1 s "
-                        "(rounds_ms_per_step, step_ms of the best round)",
+                "step_ms": [round(x, 2) for x in per_step],
+                "median_step_ms": float(np.median(per_step)),
+                "phases_ms": {k: _stats(v) for k, v in ph.items()},
+                "note": f"value = trials over the median of {E2E_ROUNDS} rounds of `steps` steps (every step timed, "
+                        "H2D/D2H included); phases_ms split each step into the host API call that streams the "
+                        "ids and runs K2 (price_layer / run_aggregate_analysis), the YLT exchange, and "
+                        "order_stats (H2D of the YLT + K3)" + ("" if workload == "c2" else
+                        f"; a {e2e_trials}-trial host sample per GPU (rate linear in trials)"),
                 "h2d_gbs": h2d / (e2e_s / e2e_steps) / 1e9,
                 "pcie_h2d_gbs_measured": pcie_gbs,
                 "frac_of_pcie": h2d / (e2e_s / e2e_steps) / 1e9 / pcie_gbs,
                 "host_pinned": host_pinned,
-                "path": "price_layer(pinned host YET) -> libaggrisk_b200 are_simulate_host -> order_stats"},
+                "path": ("run_aggregate_analysis(16 layers, host YET)" if workload == "c3" else
+                         "price_layer(pinned host YET) -> are_simulate_host") + " -> order_stats"},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "hot_set": {"hot_events": info.hot_events, "entries": info.entries,
                     "overflow_entries": info.overflow_entries, "filter_bits": info.filter_bits,
                     "smem_bytes": info.smem_bytes},
-        "precombined_k2": {"kernel_ms": pre_ms, "trials_per_s": (t1 - t0) / (pre_ms / 1e3),
-                           "bytes_formula": "trials x (12 + 8*E) (one combined value per event)",
-                           "achieved_gbs": (t1 - t0) * (12 + 8 * EVENTS) / (pre_ms / 1e3) / 1e9,
-                           "note": "different unit of work (financial terms folded per event in K1); not the headline"},
-        "c3_fused_layers": c3,
+        **side,
         "pml": list(map(float, pml_v)), "tvar": list(map(float, tvar_v)),
         "setup_seconds": {"generate": gen_s},
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and workload == "c2" and not args.no_cpu_baseline:
         # min of 3 rounds, at W = all host cores and W = 1
         cores = host_cores()
         sample = args.cpu_sample or calibrate_sample(layer, cores, 4.0)
-        cb = cpu_reference(layer, yet, sample, cores, steps=3)
+        cb = cpu_reference(layer, host_yet, sample, cores, steps=3)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         sample1 = args.cpu_sample or calibrate_sample(layer, 1, 3.0)
-        cb1 = cpu_reference(layer, yet, sample1, 1, steps=3)
+        cb1 = cpu_reference(layer, host_yet, sample1, 1, steps=3)
         line["cpu_baseline"]["w1"] = {k: cb1[k] for k in ("value", "unit", "cores", "sample")}
         line["cpu_baseline"]["host"] = host_descriptor()
     print(json.dumps(line), flush=True)
@@ -555,7 +714,14 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=["c2", "c3", "c4"], default="c2",
+                    help="c2: 1M trials per GPU (weak scaling, the headline); c3: the 16-layer portfolio over "
+                         "1M trials split across the GPUs; c4: 10M trials split across the GPUs")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="strong = --workload c4 (C4's fixed 10M trials over N GPUs)")
     args = ap.parse_args()
+    if args.scaling == "strong" and args.workload == "c2":
+        args.workload = "c4"
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
