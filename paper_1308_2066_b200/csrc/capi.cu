@@ -259,6 +259,85 @@ static int ensure_event_major(are_plan_s *p, int sms, cudaStream_t st) {
     return ARE_OK;
 }
 
+// The relay kernel's records and filter: built once per plan on its first
+// hot-set launch (exact plans only; pooled and pre-combined plans keep their
+// own kernels).  ARE_K2_RELAY=0 keeps k2_hotset (A/B).  If the records
+// cannot be allocated k2_hotset runs instead.
+static bool relay_off() {
+    static const bool off = [] {
+        const char *e = getenv("ARE_K2_RELAY");
+        return e && e[0] == '0';
+    }();
+    return off;
+}
+static uint64_t dbits(double x) {
+    uint64_t b;
+    std::memcpy(&b, &x, sizeof b);
+    return b;
+}
+// Builds the plan's relay records on first use and returns (in *filter) the
+// filter of the events that contribute under (occ_ret, occ_lim), built once
+// per distinct pair of terms (null: run k2_hotset).
+static int ensure_relay(are_plan_s *p, const DeviceInfo *di, double occ_ret, double occ_lim, cudaStream_t st,
+                        const uint32_t **filter) {
+    *filter = nullptr;
+    if (p->pool || p->precombined || relay_off()) return ARE_OK;
+    std::lock_guard<std::mutex> g(p->relay_mu);
+    if (!p->relay_tried) {
+        p->relay_tried = true;
+        const int64_t fixed = (int64_t)k2_relay_fixed_smem();
+        const int64_t avail = std::min<int64_t>(di->smem_optin, k2_max_dynamic_smem()) - fixed - 64;
+        const int64_t max_bits = (avail / 16) * 128;
+        const int64_t want = ((p->tab->row_len + 127) / 128) * 128;
+        int64_t nbits = std::max<int64_t>(std::min(want, max_bits), 128);
+        RelayBuffers rb;
+        int rc = k1_build_relay(p->pb, p->d_fin, p->tab->row_len, nbits, rb, di->sms, st);
+        // other streams may use the plan next: the records must be complete
+        if (rc == ARE_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "relay records");
+        if (rc) {
+            rb.release();
+            if (rc == ARE_ENOMEM) return ARE_OK;
+            return rc;
+        }
+        p->rnbits = nbits;
+        p->rhash_mode = nbits >= p->tab->row_len ? 0 : (p->tab->row_len <= 2 * nbits ? 1 : 2);
+        p->rsmem = (size_t)fixed + (size_t)(nbits / 8);
+        p->rb = rb;
+    }
+    if (!p->rb.rslots) return ARE_OK;
+    const uint64_t kr = dbits(occ_ret), kl = dbits(occ_lim);
+    are_plan_s::OccFilter *slot = nullptr;
+    for (auto &f : p->occf)
+        if (f.d && f.ret_bits == kr && f.lim_bits == kl) {
+            f.stamp = ++p->occ_clock;
+            *filter = f.d;
+            return ARE_OK;
+        }
+    for (auto &f : p->occf)
+        if (!slot || !f.d || (slot->d && f.stamp < slot->stamp)) slot = &f;
+    const int64_t nwords = (p->rnbits + 31) / 32;
+    if (slot->d) {
+        // an earlier launch on any stream may still read the evicted filter
+        ARE_CUDA(cudaDeviceSynchronize());
+    } else if (cudaMalloc(&slot->d, (nwords + 4) * sizeof(uint32_t)) != cudaSuccess) {
+        cudaGetLastError();
+        slot->d = nullptr;
+        return ARE_OK;  // k2_hotset runs instead
+    }
+    int rc = k1_relay_filter(p->rb, p->tab->row_len, p->rnbits, occ_ret, occ_lim, slot->d, di->sms, st);
+    if (rc == ARE_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "relay filter");
+    if (rc) {
+        cudaFree(slot->d);
+        slot->d = nullptr;
+        return rc;
+    }
+    slot->ret_bits = kr;
+    slot->lim_bits = kl;
+    slot->stamp = ++p->occ_clock;
+    *filter = slot->d;
+    return ARE_OK;
+}
+
 static void fill_args(const are_plan_s *p, K2Args &a, double occ_ret, double occ_lim, double agg_ret,
                       double agg_lim) {
     a.filter = p->pb.filter;
@@ -280,6 +359,13 @@ static void fill_args(const are_plan_s *p, K2Args &a, double occ_ret, double occ
     a.precombined = p->precombined ? 1 : 0;
     a.em = p->d_em;
     a.em_stride = p->em_stride;
+    a.rslots = nullptr;  // set with the terms' filter (ensure_relay)
+    a.rovf = p->rb.rovf;
+    a.rfilter = nullptr;
+    a.rfilter_words = p->rb.filter_words;
+    a.rnbits = (uint32_t)p->rnbits;
+    a.rhash_mode = p->rhash_mode;
+    a.rsmem = p->rsmem;
 }
 
 // K2 over trials [first, last) of ids/offsets indexed from id_base/t_base
@@ -295,8 +381,14 @@ int simulate_range(are_plan_s *p, const uint32_t *ids, int64_t id_base, int64_t 
     DeviceInfo *di;
     if ((rc = use_device(p->device, &di))) return rc;
     if ((v & 0xFF) == ARE_VARIANT_DENSE && (rc = ensure_event_major(p, di->sms, st))) return rc;
+    const uint32_t *rfilter = nullptr;
+    if ((v & 0xFF) == ARE_VARIANT_HOTSET && (rc = ensure_relay(p, di, occ_ret, occ_lim, st, &rfilter))) return rc;
     K2Args a{};
     fill_args(p, a, occ_ret, occ_lim, agg_ret, agg_lim);
+    if (rfilter) {
+        a.rslots = p->rb.rslots;
+        a.rfilter = rfilter;
+    }
     a.mean_len = mean_len;
     a.ids = ids;
     a.id_base = id_base;
@@ -595,6 +687,8 @@ int are_plan_free(are_plan_t p) {
     cudaFree(p->pb.slots);
     cudaFree(p->pb.ovf);
     cudaFree(p->pb.filter);
+    p->rb.release();
+    for (auto &f : p->occf) cudaFree(f.d);
     tables_release(p->tab);
     delete p;
     return ARE_OK;
@@ -612,6 +706,8 @@ int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ
     DeviceInfo *di;
     if ((rc = use_device(p->device, &di))) return rc;
     if ((v & 0xFF) == ARE_VARIANT_DENSE && (rc = ensure_event_major(p, di->sms, (cudaStream_t)stream))) return rc;
+    const uint32_t *rfilter = nullptr;
+    if ((v & 0xFF) == ARE_VARIANT_HOTSET && (rc = ensure_relay(p, di, occ_ret, occ_lim, (cudaStream_t)stream, &rfilter))) return rc;
     K2Args a{};
     a.mean_len = n_trials > 0 ? (double)n_occ / (double)n_trials : 0.0;
     a.ids = d_event_ids;
@@ -625,6 +721,10 @@ int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ
     a.out_base = 0;
     a.err = p->d_err;
     fill_args(p, a, occ_ret, occ_lim, agg_ret, agg_lim);
+    if (rfilter) {
+        a.rslots = p->rb.rslots;
+        a.rfilter = rfilter;
+    }
     return k2_launch(a, v, di->sms, p->smem, (cudaStream_t)stream);
 }
 
@@ -822,8 +922,14 @@ int are_simulate_host(are_plan_t p, const uint32_t *event_ids, int64_t n_occ, co
     ARE_CUDA(cudaEventRecord(w.consumed[1], w.comp));
 
     if ((v & 0xFF) == ARE_VARIANT_DENSE && (rc = ensure_event_major(p, di->sms, w.comp))) return rc;
+    const uint32_t *rfilter = nullptr;
+    if ((v & 0xFF) == ARE_VARIANT_HOTSET && (rc = ensure_relay(p, di, occ_ret, occ_lim, w.comp, &rfilter))) return rc;
     K2Args a{};
     fill_args(p, a, occ_ret, occ_lim, agg_ret, agg_lim);
+    if (rfilter) {
+        a.rslots = p->rb.rslots;
+        a.rfilter = rfilter;
+    }
     a.mean_len = (double)(offsets[last] - offsets[first]) / (double)(last - first);
     a.out = w.d_out;
     a.out_base = first;

@@ -72,6 +72,22 @@ struct are_plan_s {
     double *d_em = nullptr;
     int32_t em_stride = 0;
     bool em_tried = false;
+    // relay-kernel records and filter (k1_build_relay), built on first use
+    std::mutex relay_mu;
+    are::RelayBuffers rb;
+    int64_t rnbits = 0;
+    int rhash_mode = 0;
+    size_t rsmem = 0;
+    bool relay_tried = false;
+    // per occurrence terms: the filter of the events whose occurrence value
+    // is not +-0 (k1_relay_filter); a few recent terms kept, LRU
+    struct OccFilter {
+        uint64_t ret_bits = 0, lim_bits = 0, stamp = 0;
+        uint32_t *d = nullptr;
+    };
+    static constexpr int OCC_FILTERS = 4;
+    OccFilter occf[OCC_FILTERS];
+    uint64_t occ_clock = 0;
 };
 
 

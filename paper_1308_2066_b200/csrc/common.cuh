@@ -53,6 +53,17 @@ struct __align__(16) Entry {
     uint32_t pad;
 };
 
+// Relay-kernel record (k2_relay.cu), one per event id, 32 bytes (one 256-bit
+// load): the event's selected entries with the financial terms already
+// applied by K1 -- x0 = 0.0 + f_{j1}(x_{j1}) (the first partial sum of comb),
+// f1/f2 the 2nd/3rd entries' f_j(x_j), cnt the number of non-zero entries,
+// ovf the index in the relay overflow array of the 4th entry.
+struct __align__(32) RSlot {
+    double x0, f1, f2;
+    uint32_t cnt;
+    uint32_t ovf;
+};
+
 // Financial terms of one selected table (FinancialTerms, model.py:46-66).
 struct __align__(32) Fin {
     double rate, ret, lim, share;

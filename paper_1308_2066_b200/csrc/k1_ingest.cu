@@ -156,6 +156,105 @@ int k1_precombine_plan(PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int s
     return ARE_OK;
 }
 
+// Relay records (k2_relay.cu): the financial terms applied once per entry, in
+// the same _rn operations K2 would use, and the first partial sum 0.0 + f
+// taken here, so K2 adds f_{j2}, f_{j3}, ... in selection order exactly as
+// the reference's comb loop does (_kernel.pyx:69-76).
+__global__ void k1_relay_slots(const Slot *__restrict__ slots, const Entry *__restrict__ ovf,
+                               const Fin *__restrict__ fin, int64_t row_len, RSlot *__restrict__ rs) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < row_len;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const Slot s = slots[e];
+        const uint32_t cnt = s.meta >> 16;
+        RSlot r;
+        r.x0 = 0.0;
+        r.f1 = 0.0;
+        r.f2 = 0.0;
+        r.cnt = cnt;
+        r.ovf = cnt >= 4 ? s.ovf + 2 : 0;
+        if (cnt) r.x0 = __dadd_rn(0.0, fin_term(fin[s.meta & 0xFFFFu], s.x));
+        if (cnt >= 2) {
+            const Entry en = ovf[s.ovf];
+            r.f1 = fin_term(fin[en.j], en.x);
+        }
+        if (cnt >= 3) {
+            const Entry en = ovf[s.ovf + 1];
+            r.f2 = fin_term(fin[en.j], en.x);
+        }
+        rs[e] = r;
+    }
+}
+
+__global__ void k1_relay_ovf(const Entry *__restrict__ ovf, const Fin *__restrict__ fin, int64_t n,
+                             double *__restrict__ rovf) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const Entry en = ovf[i];
+        rovf[i] = fin_term(fin[en.j], en.x);
+    }
+}
+
+int k1_build_relay(const PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int64_t filter_bits, RelayBuffers &rb,
+                   int sms, cudaStream_t st) {
+    const int64_t n_ovf = std::max<int64_t>(pb.overflow_entries, 1);
+    if (cudaMalloc(&rb.rslots, row_len * sizeof(RSlot)) != cudaSuccess ||
+        cudaMalloc(&rb.rovf, n_ovf * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        rb.release();
+        return fail(ARE_ENOMEM, "device allocation failed while building the relay records");
+    }
+    k1_relay_slots<<<grid_for(row_len, 256, sms), 256, 0, st>>>(pb.slots, pb.ovf, d_fin, row_len, rb.rslots);
+    ARE_LAUNCHED();
+    if (pb.overflow_entries) {
+        k1_relay_ovf<<<grid_for(pb.overflow_entries, 256, sms), 256, 0, st>>>(pb.ovf, d_fin, pb.overflow_entries,
+                                                                               rb.rovf);
+        ARE_LAUNCHED();
+    }
+    rb.filter_words = (filter_bits + 31) / 32;  // the per-terms filters (k1_relay_filter)
+    return ARE_OK;
+}
+
+// Contributing events: an event whose
+// occurrence value v = clamp(comb - occ_ret, 0, occ_lim) is +-0 adds +-0 to a
+// trial sum that is never -0, so skipping it is exact, like skipping an event
+// absent from every table.  comb is evaluated from the relay record in the
+// same _rn sequence K2 uses.  One warp per filter word; bit b covers the events
+// e = b, b + nbits, ... (the relay kernel's hash).
+__global__ void k1_relay_filter_kernel(const RSlot *__restrict__ rs, const double *__restrict__ rovf, int64_t row_len,
+                                       int64_t nbits, int64_t nwords, double occ_ret, double occ_lim,
+                                       uint32_t *__restrict__ words) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t b = w * 32 + lane;
+        bool hot = false;
+        if (b < nbits)
+            for (int64_t e = b; e < row_len; e += nbits) {
+                const RSlot r = rs[e];
+                if (!r.cnt) continue;
+                double comb = r.x0;
+                if (r.cnt >= 2) comb = __dadd_rn(comb, r.f1);
+                if (r.cnt >= 3) comb = __dadd_rn(comb, r.f2);
+                for (uint32_t i = 3; i < r.cnt; ++i) comb = __dadd_rn(comb, rovf[r.ovf + i - 3]);
+                double v = __dsub_rn(comb, occ_ret);
+                if (v < 0.0) v = 0.0;
+                if (v > occ_lim) v = occ_lim;
+                hot |= !(v == 0.0);
+            }
+        const uint32_t word = __ballot_sync(0xffffffffu, hot);
+        if (lane == 0) words[w] = word;
+    }
+}
+
+int k1_relay_filter(const RelayBuffers &rb, int64_t row_len, int64_t nbits, double occ_ret, double occ_lim,
+                    uint32_t *words, int sms, cudaStream_t st) {
+    const int64_t nwords = (nbits + 31) / 32;
+    ARE_CUDA(cudaMemsetAsync(words, 0, (nwords + 4) * sizeof(uint32_t), st));
+    k1_relay_filter_kernel<<<grid_for(nwords * 32, 256, sms), 256, 0, st>>>(rb.rslots, rb.rovf, row_len, nbits, nwords,
+                                                                             occ_ret, occ_lim, words);
+    ARE_LAUNCHED();
+    return ARE_OK;
+}
+
 // ---- exclusive scan of uint32 counts (3 passes, deterministic) ------------
 static constexpr int SCAN_THREADS = 1024;
 static constexpr int SCAN_ITEMS = 4;

@@ -13,6 +13,28 @@ struct PlanBuffers {
     int64_t overflow_entries = 0;
 };
 
+// Relay-kernel buffers of a plan (k1_build_relay / k2_relay.cu).
+struct RelayBuffers {
+    RSlot *rslots = nullptr;     // row_len records
+    double *rovf = nullptr;      // fin-applied overflow values (same indexing as PlanBuffers::ovf)
+    int64_t filter_words = 0;    // words of each per-terms filter (k1_relay_filter)
+    void release() {
+        cudaFree(rslots);
+        cudaFree(rovf);
+        rslots = nullptr;
+        rovf = nullptr;
+    }
+};
+
+int k1_build_relay(const PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int64_t filter_bits, RelayBuffers &rb,
+                   int sms, cudaStream_t st);
+
+// The relay filter for one pair of occurrence terms: bit b set iff some
+// event e with hash(e) == b has an occurrence value that is not +-0 under
+// (occ_ret, occ_lim); words must hold (nbits + 31) / 32 (+4 pad) words.
+int k1_relay_filter(const RelayBuffers &rb, int64_t row_len, int64_t nbits, double occ_ret, double occ_lim,
+                    uint32_t *words, int sms, cudaStream_t st);
+
 int k1_scatter(const uint32_t *d_ids, const double *d_losses, const int64_t *d_table_offsets,
                int64_t n_tables, int64_t max_records, int64_t row_len, double *d_stacked,
                int sms, cudaStream_t st);

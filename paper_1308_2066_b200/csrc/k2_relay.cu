@@ -1,0 +1,414 @@
+// K2-R -- the relay kernel: the hot-set simulation with the in-order fold
+// moved off the streaming warps.
+//
+// Same contract and float64 sequence as k2_hotset (k2_trials.cu; reference
+// run_trials, pkg/src/aggrisk/engine/_kernel.pyx:61-118): for trial t and
+// each occurrence e in trial order
+//     comb = 0.0 + f_{j1}(x) + f_{j2}(x) + ...        (selection order)
+//     c   += clamp(comb - occ_ret, 0, occ_lim)
+//     out[t] = clamp(c - agg_ret, 0, agg_lim)
+// where f_j(x) = share_j * clamp(rate_j * x - ret_j, 0, lim_j) is evaluated
+// once per table entry by K1 (k1_relay_slots: a pure function of the entry,
+// same _rn operations), so K2 still gathers every (event, ELT) entry of a hot
+// event and sums them in selection order, but no longer re-evaluates the
+// financial terms per occurrence.
+//
+// One persistent CTA of 1024 threads per SM:
+//   * warps 0..30 ("producers") each own trials first + b*31 + w, +31*grid,
+//     ...: they stream the trial's ids (32-id coalesced rows, two 128-id
+//     chunks in flight), test each id against the shared-memory filter,
+//     append the hot ones in trial order to a per-warp queue, and per 32
+//     queued events gather one 32-byte record per lane (one 256-bit L2 load:
+//     the event's first partial sum, its 2nd and 3rd entries, the count) and
+//     compute the event's occurrence value.  The 32 values go to the warp's
+//     ring in shared memory -- one STS per lane -- instead of being folded;
+//   * warp 31 ("fold") folds: lane l consumes producer l's ring, adding each
+//     batch's 32 values to its trial's running sum strictly in order (+0.0 for
+//     lanes past a trial's last event: c >= +0, so that is exact), and writes
+//     out[t] at the batch that ends the trial.  One warp instruction advances
+//     31 trials' chains, where k2_hotset spent 16 LDS.128 + 32 dependent DADD
+//     of a whole warp on every batch.
+// Producer and fold synchronise through two mbarriers per ring slot (full:
+// the producer's 32 lanes arrive after storing; empty: the fold lane arrives
+// after reading), release/acquire at CTA scope without a fence; a ring holds
+// KR_NB batches.
+#include "k2_trials.cuh"
+
+namespace are {
+
+// Build-time variants (A/B experiments; the defaults are the measured choice).
+#ifndef ARE_KR_NF
+#define ARE_KR_NF 1        // fold warps
+#endif
+#ifndef ARE_KR_NB
+#define ARE_KR_NB 2        // ring slots (batches) per producer
+#endif
+#ifndef ARE_KR_ROWDRAIN
+#define ARE_KR_ROWDRAIN 0  // drain the queue after every row (64-entry queue) instead of every two
+#endif
+#ifndef ARE_KR_EXP
+#define ARE_KR_EXP 0       // timing experiments only (results are wrong when != 0)
+#endif
+#ifndef ARE_KR_PF
+#define ARE_KR_PF 0        // L2 bulk prefetch of ids: 0 = none (measured best), 1 = chunks ch+4..ch+6 every 3 chunks, 2 = the next trial at trial start
+#endif
+static constexpr int KR_NF = ARE_KR_NF;
+static constexpr int KR_NP = (K2R_THREADS / 32 - KR_NF) / KR_NF * KR_NF;  // producer warps
+static constexpr int KR_PF = KR_NP / KR_NF;                                // producers per fold warp
+static constexpr int KR_QCAP = ARE_KR_ROWDRAIN ? 64 : 128;  // per-producer hot queue (< 32 pending + the rows between drains)
+static constexpr int KR_NB = ARE_KR_NB;                     // batches per ring
+static constexpr int KR_RSTRIDE = KR_NB * 32 + 2;  // doubles per ring (+16 B: the fold's 32 lanes hit distinct banks)
+
+size_t k2_relay_fixed_smem() {
+    return (size_t)KR_NP * KR_QCAP * sizeof(uint32_t) + (size_t)KR_NP * KR_RSTRIDE * sizeof(double) +
+           (size_t)2 * 32 * KR_NB * sizeof(uint64_t) + (size_t)32 * KR_NB * sizeof(uint32_t);
+}
+
+// A gathered relay record kept exactly as loaded (four doubles; count and
+// overflow index decoded where used), so the loop-carried pending batch can
+// live in the load's own destination registers (no copy of an in-flight load).
+struct RRaw {
+    double x0, f1, f2, m;
+};
+__device__ __forceinline__ RRaw ld_rslot(const RSlot *p, uint64_t policy) {
+    RRaw r;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=d"(r.x0), "=d"(r.f1), "=d"(r.f2), "=d"(r.m)
+                 : "l"(p), "l"(policy));
+    return r;
+}
+// mbarrier helpers (shared::cta).  arrive has release and test/try_wait
+// acquire semantics at CTA scope; neither waits for the thread's in-flight
+// global loads (a fence would: MEMBAR.CTA stalls until the id stream's
+// outstanding LDGs return).
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint32_t a, uint32_t parity) {
+    uint32_t r;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(r)
+        : "r"(a), "r"(parity)
+        : "memory");
+    return r != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+template <int HASH>
+__device__ __forceinline__ uint32_t relay_hash(uint32_t e, uint32_t nbits) {
+    if (HASH == 0) return e;
+    if (HASH == 1) return min(e, e - nbits);
+    return e % nbits;
+}
+
+// The fold warp: lane l < KR_NP consumes producer l's batches.  Batch h of
+// a producer sits in ring slot h % KR_NB; full[slot] completes its phase
+// h / KR_NB when the producer's 32 lanes have stored it, empty[slot] when the
+// fold lane has read it.
+__device__ __forceinline__ void relay_fold(const K2Args &a, int fw, const double *s_ring, uint32_t full0,
+                                           uint32_t empty0, const uint32_t *s_end) {
+    const int lane = threadIdx.x & 31;
+    const int64_t W = (int64_t)gridDim.x * KR_NP;
+    const int me = fw * KR_PF + (lane < KR_PF ? lane : 0);  // the producer this lane folds for
+    int64_t t = lane < KR_PF ? a.first + (int64_t)blockIdx.x * KR_NP + me : a.last;
+    const double *ring = s_ring + me * KR_RSTRIDE;
+    const uint32_t full = full0 + me * KR_NB * 8, empty = empty0 + me * KR_NB * 8;
+    const double agg_ret = a.agg_ret, agg_lim = a.agg_lim;
+    double c = 0.0;
+    uint32_t head = 0;
+    while (__any_sync(0xffffffffu, t < a.last)) {
+        const uint32_t slot = head & (KR_NB - 1);
+        bool ready = false;
+        if (t < a.last) ready = mbar_test(full + slot * 8, (head / KR_NB) & 1);
+        if (!__any_sync(0xffffffffu, ready)) {
+            __nanosleep(32);
+            continue;
+        }
+        if (ready) {
+            const double2 *r2 = reinterpret_cast<const double2 *>(ring + slot * 32);
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                double2 w[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) w[i] = r2[4 * g + i];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    c = __dadd_rn(c, w[i].x);
+                    c = __dadd_rn(c, w[i].y);
+                }
+            }
+            const uint32_t end = s_end[me * KR_NB + slot];
+            mbar_arrive(empty + slot * 8);  // the slot's values are in registers
+            ++head;
+            if (end) {
+                a.out[t - a.out_base] = clamp_ref(__dsub_rn(c, agg_ret), agg_lim);
+                c = 0.0;
+                t += W;
+            }
+        }
+    }
+}
+
+template <int HASH, bool CHECK>
+__global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    // the filter at offset 0 (its LDS addresses need no base register)
+    uint32_t *s_filter = reinterpret_cast<uint32_t *>(smem);
+    uint32_t *s_q = s_filter + a.filter_words;
+    double *s_ring = reinterpret_cast<double *>(s_q + KR_NP * KR_QCAP);
+    uint64_t *s_bar = reinterpret_cast<uint64_t *>(s_ring + KR_NP * KR_RSTRIDE);  // full[32][NB], empty[32][NB]
+    uint32_t *s_end = reinterpret_cast<uint32_t *>(s_bar + 2 * 32 * KR_NB);
+    const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(s_bar);
+    const uint32_t empty0 = full0 + 32 * KR_NB * 8;
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.filter);
+        uint4 *dst = reinterpret_cast<uint4 *>(s_filter);
+        const int n4 = (int)(a.filter_words >> 2);
+        for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+        if (threadIdx.x < KR_NP * KR_NB) {
+            mbar_init(full0 + threadIdx.x * 8, 32);  // the producer's 32 lanes
+            mbar_init(empty0 + threadIdx.x * 8, 1);  // its fold lane
+        }
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp >= KR_NP) {
+        if (warp < KR_NP + KR_NF) relay_fold(a, warp - KR_NP, s_ring, full0, empty0, s_end);
+        return;
+    }
+    const uint32_t my_full = full0 + warp * KR_NB * 8, my_empty = empty0 + warp * KR_NB * 8;
+
+    uint32_t *q = s_q + warp * KR_QCAP;
+    const uint32_t q_saddr = (uint32_t)__cvta_generic_to_shared(q);
+    double *ring = s_ring + warp * KR_RSTRIDE;
+    const uint32_t lt = lanemask_lt();
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
+    const uint32_t nbits = a.nbits, last_id = a.row_len - 1;
+    const double occ_ret = a.occ_ret, occ_lim = a.occ_lim;
+    const uint32_t *const ids = a.ids;
+    const int64_t W = (int64_t)gridDim.x * KR_NP;
+    uint32_t emax = 0;
+    const uint32_t pad = cold_pad(s_filter, a.filter_words, nbits, a.row_len);
+    uint32_t seq = 0;  // batches published (uniform)
+
+    // publish one batch of 32 occurrence values (lanes past the batch: +0.0)
+    auto push = [&](double v, uint32_t end) {
+        const uint32_t slot = seq & (KR_NB - 1), use = seq / KR_NB;
+        if (use) mbar_wait(my_empty + slot * 8, (use - 1) & 1);  // the fold has read the slot's last batch
+        ring[slot * 32 + lane] = v;
+        if (lane == 0) s_end[warp * KR_NB + slot] = end;
+        mbar_arrive(my_full + slot * 8);
+        ++seq;
+    };
+    // occurrence value of this lane's gathered event (slot 0 -- empty -- for
+    // lanes past the batch: comb = +0.0, v = clamp(-occ_ret) = +-0)
+    auto value = [&](const RRaw &s) -> double {
+        const uint32_t cnt = (uint32_t)__double2loint(s.m);
+        double comb = s.x0;
+        if (cnt >= 2u) comb = __dadd_rn(comb, s.f1);
+        if (cnt >= 3u) {
+            comb = __dadd_rn(comb, s.f2);
+            const uint32_t ovf = (uint32_t)__double2hiint(s.m);
+#pragma unroll 1
+            for (uint32_t i = 3; i < cnt; ++i) comb = __dadd_rn(comb, a.rovf[ovf + i - 3]);
+        }
+        return clamp_ref(__dsub_rn(comb, occ_ret), occ_lim);
+    };
+    auto gather = [&](uint32_t qh, uint32_t n) -> RRaw {
+        const uint32_t e = q[(qh + lane) & (KR_QCAP - 1)];
+#if ARE_KR_EXP == 4  // timing experiment: every gather from a 512 KB window
+        return ld_rslot(a.rslots + ((uint32_t)lane < n ? (e & 0x3FFFu) : 0u), pol_keep);
+#elif ARE_KR_EXP == 5  // timing experiment: 16-byte gathers of the same records
+        {
+            const uint4 r = ld_stream_u4(reinterpret_cast<const uint32_t *>(a.rslots + ((uint32_t)lane < n ? e : 0u)), pol_keep);
+            return RRaw{__hiloint2double((int)r.y, (int)r.x), 0.0, 0.0, __hiloint2double((int)r.w, (int)r.z)};
+        }
+#endif
+        return ld_rslot(a.rslots + ((uint32_t)lane < n ? e : 0u), pol_keep);
+    };
+
+    int64_t t = a.first + (int64_t)blockIdx.x * KR_NP + warp;
+    int64_t lo = 0, hi = 0;
+    if (t < a.last) {
+        lo = a.offsets[t - a.t_base];
+        hi = a.offsets[t - a.t_base + 1];
+    }
+#if ARE_KR_PF == 2
+    int64_t nlo = 0, nhi = 0;  // the next trial's bounds: known one trial ahead
+    if (t + W < a.last) {
+        nlo = a.offsets[t + W - a.t_base];
+        nhi = a.offsets[t + W - a.t_base + 1];
+    }
+#endif
+    for (; t < a.last; t += W) {
+#if ARE_KR_PF == 2
+        const int64_t tnn = t + 2 * W;
+        int64_t nnlo = 0, nnhi = 0;
+        if (tnn < a.last) {  // bounds two trials ahead, in flight during this trial
+            nnlo = a.offsets[tnn - a.t_base];
+            nnhi = a.offsets[tnn - a.t_base + 1];
+        }
+        if (lane == 0 && nhi > nlo) {  // the next trial's ids to L2 (16-byte aligned span)
+            const uintptr_t b0 = reinterpret_cast<uintptr_t>(ids + (nlo - a.id_base)) & ~(uintptr_t)15;
+            const uintptr_t b1 = (reinterpret_cast<uintptr_t>(ids + (nhi - a.id_base)) + 15) & ~(uintptr_t)15;
+            prefetch_l2_bulk(reinterpret_cast<const void *>(b0), (uint32_t)(b1 - b0));
+        }
+#else
+        const int64_t tn = t + W;
+        int64_t nlo = 0, nhi = 0;
+        if (tn < a.last) {  // next trial's bounds, in flight during this trial
+            nlo = a.offsets[tn - a.t_base];
+            nhi = a.offsets[tn - a.t_base + 1];
+        }
+#endif
+        const int64_t rlo = lo - a.id_base;
+        const uint32_t len = (uint32_t)(hi - lo);
+        const uint32_t skew = (uint32_t)((reinterpret_cast<uintptr_t>(ids + rlo) >> 2) & 31);
+        const uint32_t *p = ids + (rlo - skew) + lane;
+        uint32_t rel = (uint32_t)lane - skew;
+        const int nchunks = (int)((len + skew + 127) >> 7);
+        uint32_t qh = 0, qt = 0;
+        bool pending = false;
+        RRaw ps{0.0, 0.0, 0.0, 0.0};
+
+        uint32_t r0[4], r1[4], r2[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r0[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream, pad);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r1[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream, pad);
+
+        auto step = [&](uint32_t (&cur)[4], uint32_t (&fut)[4]) {
+            const uint32_t rel0 = rel - (uint32_t)lane + 256u;  // start of the chunk loaded now, trial-relative
+            if ((int32_t)rel0 >= 0 && rel0 + 128u <= len) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) fut[k] = ld_stream_u32(p + 256 + 32 * k, pol_stream);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 256 + 32 * k, rel + 256 + 32 * k, len, pol_stream, pad);
+            }
+            uint32_t ev[4], word[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t e = cur[k];
+                if (CHECK) {
+                    emax = max(emax, e);
+                    e = min(e, last_id);
+                }
+                ev[k] = e;
+                word[k] = s_filter[relay_hash<HASH>(e, nbits) >> 5];
+            }
+            constexpr int RPD = ARE_KR_ROWDRAIN ? 1 : 2;  // rows per drain check
+#pragma unroll
+            for (int half = 0; half < 4 / RPD; ++half) {
+#pragma unroll
+                for (int k = RPD * half; k < RPD * half + RPD; ++k) {
+                    const bool hot = (word[k] >> (relay_hash<HASH>(ev[k], nbits) & 31)) & 1u;
+#if ARE_KR_EXP == 1  // timing experiment: filter only
+                    emax += hot;
+                    continue;
+#endif
+                    const uint32_t b = ballot_full(hot);
+                    st_shared_if(q_saddr + (((qt + __popc(b & lt)) & (KR_QCAP - 1)) << 2), ev[k], hot);
+                    qt += __popc(b);
+                }
+                __syncwarp();
+                while (qt - qh >= 32u) {
+#if ARE_KR_EXP == 2  // timing experiment: filter + append, no batches
+                    qh += 32u;
+                    continue;
+#endif
+                    // the pending batch's value first, then the new gather into
+                    // the same registers: no register copy of an in-flight load
+                    const double v = value(ps);
+#if ARE_KR_EXP == 3  // timing experiment: no push
+                    ps = gather(qh, 32u);
+                    if (v == 12345.0) emax++;
+                    pending = true;
+                    qh += 32u;
+                    continue;
+#endif
+                    ps = gather(qh, 32u);
+                    if (pending) push(v, 0u);
+                    pending = true;
+                    qh += 32u;
+                }
+            }
+            p += 128;
+            rel += 128;
+        };
+        for (int ch = 0; ch < nchunks; ch += 3) {
+#if ARE_KR_PF == 1
+            if (lane == 0) {  // chunks ch+4 .. ch+6 to L2 ahead of their row loads
+                const uint32_t a0 = rel - (uint32_t)lane + 512u;
+                if ((int32_t)a0 < (int32_t)len) prefetch_l2_bulk(p - lane + 512, 1536);
+            }
+#endif
+            step(r0, r2);
+            if (ch + 1 >= nchunks) break;
+            step(r1, r0);
+            if (ch + 2 >= nchunks) break;
+            step(r2, r1);
+        }
+        const uint32_t n = qt - qh;  // final partial batch
+        const double v = value(ps);
+        if (n) {
+            ps = gather(qh, n);
+            if (pending) push(v, 0u);
+            push(value(ps), 1u);
+        } else {
+            push(pending ? v : 0.0, 1u);
+        }
+        lo = nlo;
+        hi = nhi;
+#if ARE_KR_PF == 2
+        nlo = nnlo;
+        nhi = nnhi;
+#endif
+    }
+#if ARE_KR_EXP
+    if (emax == 0xFFFFFFFFu) a.out[0] = 1.0;
+#endif
+    if (CHECK && __any_sync(0xffffffffu, emax > last_id) && lane == 0) atomicOr(a.err, 1u);
+}
+
+int k2_relay_prepare() {
+    ARE_CUDA(cudaFuncSetAttribute(k2_relay<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
+    ARE_CUDA(cudaFuncSetAttribute(k2_relay<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
+    ARE_CUDA(cudaFuncSetAttribute(k2_relay<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
+    ARE_CUDA(cudaFuncSetAttribute(k2_relay<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
+    ARE_CUDA(cudaFuncSetAttribute(k2_relay<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
+    ARE_CUDA(cudaFuncSetAttribute(k2_relay<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
+    return ARE_OK;
+}
+
+int k2_relay_launch(const K2Args &a, bool check, int sms, size_t smem_bytes, cudaStream_t st) {
+    if (a.last <= a.first) return ARE_OK;
+    const int64_t trials = a.last - a.first;
+    int64_t g = (trials + KR_NP - 1) / KR_NP;
+    if (g > sms) g = sms;  // persistent: one CTA per SM (the filter fills shared memory)
+    const dim3 grid((unsigned)g), block(K2R_THREADS);
+    const int sel = a.hash_mode * 2 + (check ? 1 : 0);
+    switch (sel) {
+        case 0: k2_relay<0, false><<<grid, block, smem_bytes, st>>>(a); break;
+        case 1: k2_relay<0, true><<<grid, block, smem_bytes, st>>>(a); break;
+        case 2: k2_relay<1, false><<<grid, block, smem_bytes, st>>>(a); break;
+        case 3: k2_relay<1, true><<<grid, block, smem_bytes, st>>>(a); break;
+        case 4: k2_relay<2, false><<<grid, block, smem_bytes, st>>>(a); break;
+        default: k2_relay<2, true><<<grid, block, smem_bytes, st>>>(a); break;
+    }
+    ARE_LAUNCHED();
+    return ARE_OK;
+}
+
+}  // namespace are

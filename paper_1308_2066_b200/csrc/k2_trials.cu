@@ -770,6 +770,7 @@ int k2_prepare(int device) {
                                   (int)dense_coop_smem(32)));
     ARE_CUDA(cudaFuncSetAttribute(k2_dense_coop<DENSE_WARPS, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)dense_coop_smem(32)));
+    if ((rc = k2_relay_prepare())) return rc;
     if ((rc = k2_layers_prepare())) return rc;
     return k2_layers_pre_prepare();
 }
@@ -829,6 +830,15 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
     if (g > sms) g = sms;  // persistent: one CTA per SM (the filter fills shared memory)
     const dim3 grid((unsigned)g), block(K2_THREADS);
     const int sel = a.hash_mode * 2 + (check ? 1 : 0);
+    if (a.rslots && !a.precombined && !use_pair(a.mean_len)) {
+        // the relay kernel, over its own filter
+        K2Args b = a;
+        b.filter = a.rfilter;
+        b.filter_words = a.rfilter_words;
+        b.nbits = a.rnbits;
+        b.hash_mode = a.rhash_mode;
+        return k2_relay_launch(b, check, sms, a.rsmem, st);
+    }
     if (a.precombined)
         launch_hotset<true>(a, sel, grid, block, smem_bytes, st);
     else

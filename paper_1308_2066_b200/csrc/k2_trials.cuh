@@ -40,10 +40,21 @@ struct K2Args {
     // mean occurrences per trial of the launch (host estimate): short trials
     // run the paired kernel (k2_pair), long ones k2_hotset
     double mean_len;
+    // relay kernel (k2_relay.cu): its records, fin-applied overflow values
+    // and its own filter (its fixed shared memory differs from k2_hotset's)
+    const RSlot *rslots = nullptr;
+    const double *rovf = nullptr;
+    const uint32_t *rfilter = nullptr;
+    int64_t rfilter_words = 0;
+    uint32_t rnbits = 0;
+    int32_t rhash_mode = 0;
+    size_t rsmem = 0;
 };
 
 // Threads per CTA of the hot-set kernel (one persistent CTA per SM).
 constexpr int K2_THREADS = 1024;
+// Threads per CTA of the relay kernel: 31 producer warps + 1 fold warp.
+constexpr int K2R_THREADS = 1024;
 
 // Fused multi-layer kernel (k2_layers.cu): 16 warps per CTA, up to 16 layers
 // per launch over one ELT pool of up to 64 tables.
@@ -83,6 +94,9 @@ inline int k2_max_dynamic_smem() { return 227 * 1024; }
 size_t k2_hotset_fixed_smem(int n_sel);
 int k2_prepare(int device);
 int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStream_t st);
+size_t k2_relay_fixed_smem();
+int k2_relay_prepare();
+int k2_relay_launch(const K2Args &a, bool check, int sms, size_t smem_bytes, cudaStream_t st);
 size_t k2_layers_fixed_smem(int n_sel);
 int k2_layers_prepare();
 int k2_layers_launch(const K2Args &a, const K2Layers &L, bool check, int sms, size_t smem_bytes, cudaStream_t st);

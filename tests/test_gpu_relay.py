@@ -1,0 +1,85 @@
+"""The relay kernel (csrc/k2_relay.cu) against the reference kernel.
+
+k2_relay skips every event whose occurrence value is +-0 under the launch's
+occurrence terms (the per-terms "contributing" filter, k1_relay_filter) and
+folds on a separate warp; the YLT must still be bit-identical to the
+reference run_trials (pkg/src/aggrisk/engine/_kernel.pyx:61-118).  These
+cases move the occurrence retention across the loss distribution (from
+"every hot event contributes" to "almost none does"), reuse one plan for
+more distinct terms than the per-plan filter cache holds (eviction path), and
+mix multi-table events (records with inline 2nd/3rd entries and overflow
+beyond).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1308_2066_b200.direct_access import TableSet
+from paper_1308_2066_b200.engine import price_layer
+from paper_1308_2066_b200.portfolio import EventLossTable, FinancialTerms, LayerTerms
+from paper_1308_2066_b200.synth import GeneratorSpec, generate_elt, generate_yet
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle(yet, stacked, fin, terms):
+    out = np.empty(yet.trial_count)
+    oracle.run_trials_port(yet.event_ids, yet.offsets, stacked, np.arange(stacked.shape[0], dtype=np.int64),
+                           *fin, terms.occ_retention, terms.occ_limit, terms.agg_retention, terms.agg_limit,
+                           0, 0, yet.trial_count, out)
+    return out
+
+
+@pytest.fixture(scope="module")
+def case():
+    # long trials (the relay kernel runs above 320 occurrences per trial) over
+    # a catalog larger than the shared-memory filter, 6 ELTs with overlap so
+    # some events sit in 4+ tables (overflow entries beyond the record)
+    spec = GeneratorSpec(seed=77, catalog_size=2_000_000, trial_count=3_000, events_per_trial_range=(400, 1500),
+                         elt_count=6, elt_size_range=(150_000, 400_000))
+    yet = generate_yet(spec)
+    elts = []
+    for i in range(spec.elt_count):
+        e = generate_elt(spec, i)
+        terms = FinancialTerms(exchange_rate=1.0 + 0.1 * i, event_retention=20.0 * i, event_limit=5_000.0 + 500 * i,
+                               share=1.0 - 0.05 * i)
+        elts.append(EventLossTable(e.catalog_size, e.event_ids, e.losses, terms))
+    tset = TableSet.from_elts(elts)
+    stacked = oracle.dense_tables(elts, spec.catalog_size)
+    fin = [np.array([getattr(e.terms, f) for e in elts], dtype=np.float64)
+           for f in ("exchange_rate", "event_retention", "event_limit", "share")]
+    counts = (stacked[:, 1:] != 0).sum(axis=0)
+    assert counts.max() >= 4, "the case must include events in 4+ tables"
+    return yet, elts, tset, stacked, fin
+
+
+OCC_TERMS = [(0.0, math.inf), (500.0, 10_000.0), (2_000.0, 3_000.0), (4_000.0, math.inf), (9_000.0, 1.0),
+             (0.0, 250.0), (1e12, math.inf)]
+
+
+def test_occurrence_terms_sweep_and_filter_eviction(case):
+    yet, elts, tset, stacked, fin = case
+    for rounds in range(2):  # the second round re-meets evicted and cached filters
+        for occ_ret, occ_lim in OCC_TERMS:
+            terms = LayerTerms(occ_ret, occ_lim, 1_000.0, 2e6)
+            got, lookups = price_layer(yet, tset, None, terms)
+            want = _oracle(yet, stacked, fin, terms)
+            assert got.tobytes() == want.tobytes(), (rounds, occ_ret, occ_lim)
+            assert lookups == len(elts) * yet.event_ids.size
+
+
+def test_kernel_paths_agree_bitwise(case):
+    """AUTO (the relay kernel here) against the dense literal loop, which
+    performs every lookup: both bit-identical to the reference."""
+    yet, elts, tset, stacked, fin = case
+    from paper_1308_2066_b200.engine import EngineConfig
+
+    terms = LayerTerms(700.0, 8_000.0, 5_000.0, 1e5)
+    hot, _ = price_layer(yet, tset, None, terms)
+    dense, _ = price_layer(yet, tset, None, terms, EngineConfig(variant="dense"))
+    assert hot.tobytes() == dense.tobytes() == _oracle(yet, stacked, fin, terms).tobytes()
