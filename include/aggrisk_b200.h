@@ -223,6 +223,19 @@ int are_order_stats_device(const double *d_losses, int64_t n,
 int are_order_stats_host(const double *losses, int64_t n,
                          const double *rps, int64_t n_rp,
                          double *pml_out, double *tvar_out);
+/* are_order_stats_device plus the table's mean and maximum from the same
+ * tail pass: mean_max_out[0] = sum / n (double-double sum), mean_max_out[1] =
+ * max (NaN if any loss is NaN), as the pricing service reports them
+ * (service.py:237-238). */
+int are_order_stats_summary_device(const double *d_losses, int64_t n,
+                                   const double *rps, int64_t n_rp,
+                                   double *pml_out, double *tvar_out,
+                                   double *mean_max_out, void *stream);
+/* PML only, for many return periods at once (ep_curve, metrics.py:97-115):
+ * one device radix sort of the order-preserving keys, then one gather. */
+int are_pml_many_device(const double *d_losses, int64_t n,
+                        const double *rps, int64_t n_rp,
+                        double *pml_out, void *stream);
 /* portfolio_rollup (metrics.py:118-133): d_out[t] = ((y0[t] + y1[t]) + ...). */
 int are_rollup_device(const double *const *d_ylts, int64_t n_layers, int64_t n,
                       double *d_out, void *stream);

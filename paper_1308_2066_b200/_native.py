@@ -102,6 +102,8 @@ SIGNATURES = {
         ctypes.c_int, [_P, _I64, _P, _I64, _I64, _P, _I64, _I64, ctypes.POINTER(YetReport), _P]),
     "are_order_stats_device": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _P]),
     "are_order_stats_host": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P]),
+    "are_order_stats_summary_device": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _P, _P]),
+    "are_pml_many_device": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P]),
     "are_rollup_device": (ctypes.c_int, [_P, _I64, _I64, _P, _P]),
     # multi-GPU group (capi_group.cu)
     "are_init": (ctypes.c_int, [ctypes.c_int]),

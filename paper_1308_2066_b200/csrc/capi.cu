@@ -168,13 +168,30 @@ static int ws_reserve(Workspace &w, int64_t ids, int64_t offs, int64_t outs, boo
     return ARE_OK;
 }
 
+// Page-locked pointers seen before: the e2e path asks on every call, and a
+// driver query per call can wait behind other clients of the driver (NVML
+// sampling).  Only positive answers are cached: a stale entry (freed, then
+// reused as pageable memory) would still copy correctly, cudaMemcpyAsync
+// accepts pageable memory.
+static std::mutex g_pin_mu;
+static const void *g_pinned[64];
+static int g_pinned_next = 0;
 bool is_pinned(const void *p) {
+    {
+        std::lock_guard<std::mutex> g(g_pin_mu);
+        for (const void *q : g_pinned)
+            if (q == p) return true;
+    }
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
-    return a.type == cudaMemoryTypeHost;
+    if (a.type != cudaMemoryTypeHost) return false;
+    std::lock_guard<std::mutex> g(g_pin_mu);
+    g_pinned[g_pinned_next] = p;
+    g_pinned_next = (g_pinned_next + 1) % 64;
+    return true;
 }
 
 // Exactness precondition of the hot-set kernel (DESIGN.md "Zero-skip
@@ -445,6 +462,11 @@ int are_host_register(void *ptr, int64_t bytes) {
 int are_host_is_pinned(const void *ptr) { return is_pinned(ptr) ? 1 : 0; }
 
 int are_host_unregister(void *ptr) {
+    {
+        std::lock_guard<std::mutex> g(g_pin_mu);
+        for (const void *&q : g_pinned)
+            if (q == ptr) q = nullptr;
+    }
     cudaError_t e = cudaHostUnregister(ptr);
     if (e != cudaSuccess && e != cudaErrorHostMemoryNotRegistered) return cuda_fail(e, "cudaHostUnregister");
     cudaGetLastError();
@@ -1005,6 +1027,25 @@ int are_order_stats_device(const double *d_losses, int64_t n, const double *rps,
     DeviceInfo *di;
     if ((rc = use_device(dev, &di))) return rc;
     return k3_order_stats(d_losses, n, rps, n_rp, pml_out, tvar_out, di->sms, (cudaStream_t)stream);
+}
+
+int are_order_stats_summary_device(const double *d_losses, int64_t n, const double *rps, int64_t n_rp,
+                                   double *pml_out, double *tvar_out, double *mean_max_out, void *stream) {
+    int dev, rc;
+    if ((rc = current_device(&dev))) return rc;
+    DeviceInfo *di;
+    if ((rc = use_device(dev, &di))) return rc;
+    if (!mean_max_out) return fail(ARE_EINVAL, "null summary output");
+    return k3_order_stats(d_losses, n, rps, n_rp, pml_out, tvar_out, di->sms, (cudaStream_t)stream, mean_max_out);
+}
+
+int are_pml_many_device(const double *d_losses, int64_t n, const double *rps, int64_t n_rp, double *pml_out,
+                        void *stream) {
+    int dev, rc;
+    if ((rc = current_device(&dev))) return rc;
+    DeviceInfo *di;
+    if ((rc = use_device(dev, &di))) return rc;
+    return k3_pml_sorted(d_losses, n, rps, n_rp, pml_out, di->sms, (cudaStream_t)stream);
 }
 
 int are_order_stats_host(const double *losses, int64_t n, const double *rps, int64_t n_rp, double *pml_out,

@@ -26,6 +26,7 @@
 #include "k3_order_stats.cuh"
 
 #include <cooperative_groups.h>
+#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -82,6 +83,7 @@ struct K3Params {
     int64_t rank[K3_GROUP];    // 1-based ranks k
     int64_t m_tail[K3_GROUP];  // n - k + 1
     int n_rp;
+    int summary;               // also the mean and the maximum (slot n_rp of the tail pass)
 };
 
 // Device workspace of one K3 call; cleared (cudaMemsetAsync) before launch.
@@ -89,6 +91,7 @@ struct K3Work {
     unsigned int hist[3][K3_GROUP][K3_BINS];  // triple-buffered pass histograms
     unsigned int bar_count, bar_gen, done, pad;
     double res[2][K3_GROUP];                  // pml, tvar (output)
+    double summary[2];                        // mean, max (output, when requested)
 };
 
 __global__ void __launch_bounds__(K3_THREADS, 2) k3_select(const double *__restrict__ x, int64_t n, const K3Params prm,
@@ -226,19 +229,25 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k3_select(const double *__restr
         }
     }
     // tail: sum and count of losses strictly above each PML key, K3_TAIL
-    // return periods per sweep
-    for (int r0 = 0; r0 < R; r0 += K3_TAIL) {
+    // return periods per sweep.  The summary (mean, max) rides along as slot
+    // R: key 0 lies below every loss (NaN included), so it sums them all, and
+    // the sweep that holds it also tracks the largest key.
+    const int RT = R + (prm.summary ? 1 : 0);
+    uint64_t kmax = 0;
+    for (int r0 = 0; r0 < RT; r0 += K3_TAIL) {
         uint64_t kp[K3_TAIL];
         DD acc[K3_TAIL];
         unsigned long long above[K3_TAIL];
 #pragma unroll
         for (int r = 0; r < K3_TAIL; ++r) {
-            kp[r] = r0 + r < R ? s_prefix[r0 + r] : ~0ull;  // ~0: nothing is above
+            kp[r] = r0 + r < R ? s_prefix[r0 + r] : (r0 + r == R && prm.summary ? 0ull : ~0ull);  // ~0: nothing is above
             acc[r] = DD{0.0, 0.0};
             above[r] = 0;
         }
+        const bool track_max = prm.summary && R >= r0 && R < r0 + K3_TAIL;
         auto tail = [&](double v) {
             const uint64_t k = order_key(v);
+            if (track_max) kmax = max(kmax, k);
 #pragma unroll
             for (int r = 0; r < K3_TAIL; ++r)
                 if (k > kp[r]) {
@@ -274,11 +283,24 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k3_select(const double *__restr
                     c = s_cnt[lane][r];
                 }
                 dd_warp_reduce(a, c);
-                if (lane == 0 && r0 + r < R)
+                if (lane == 0 && r0 + r < RT)
                     part[(int64_t)(r0 + r) * gridDim.x + blockIdx.x] = TailPartial{a.hi, a.lo, c, 0};
             }
         }
         __syncthreads();
+    }
+    if (prm.summary) {  // the CTA's largest key, next to its summary partial
+        unsigned long long m = kmax;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) s_cnt[warp][0] = m;
+        __syncthreads();
+        if (warp == 0) {
+            m = lane < K3_THREADS / 32 ? s_cnt[lane][0] : 0ull;
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) part[(int64_t)R * gridDim.x + blockIdx.x].pad = m;
+        }
     }
     // the last CTA to finish combines the partials
     __threadfence();
@@ -326,6 +348,22 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k3_select(const double *__restr
             w->res[1][r] = __ddiv_rn(total, (double)m);
         }
     }
+    if (prm.summary && warp == K3_GROUP) {  // mean and max of every loss
+        DD s = {0.0, 0.0};
+        unsigned long long ab = 0, km = 0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) {
+            const TailPartial pp = part[(int64_t)R * gridDim.x + b];
+            dd_merge(s, DD{pp.hi, pp.lo});
+            km = max(km, pp.pad);
+        }
+        dd_warp_reduce(s, ab);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) km = max(km, __shfl_xor_sync(0xffffffffu, km, o));
+        if (lane == 0) {
+            w->summary[0] = __ddiv_rn(__dadd_rn(s.hi, s.lo), (double)n);
+            w->summary[1] = key_value(km);
+        }
+    }
 }
 
 __global__ void k3_rollup(const double *const *__restrict__ ylts, int n_layers, int first_chunk,
@@ -354,13 +392,13 @@ struct K3Cache {
     std::mutex mu;
     K3Work *d_work = nullptr;
     TailPartial *d_part = nullptr;
-    double *h_res = nullptr;  // pinned [2][K3_GROUP]
+    double *h_res = nullptr;  // pinned [2][K3_GROUP] + mean, max
     int grid = 0;
 };
 static K3Cache g_k3[64];
 
 int k3_order_stats(const double *d_x, int64_t n, const double *rps, int64_t n_rp, double *pml_out,
-                   double *tvar_out, int sms, cudaStream_t st) {
+                   double *tvar_out, int sms, cudaStream_t st, double *summary) {
     if (n <= 0) return fail(ARE_EINVAL, "empty year loss table");
     if (n >= (int64_t)0xFFFFFFFFll) return fail(ARE_EINVAL, "year loss table too long for K3");
     int dev;
@@ -375,12 +413,13 @@ int k3_order_stats(const double *d_x, int64_t n, const double *rps, int64_t n_rp
         if (per_sm < 1) return fail(ARE_ECUDA, "K3 does not fit on an SM");
         c.grid = sms * std::min(per_sm, 2);
         ARE_CUDA(cudaMalloc(&c.d_work, sizeof(K3Work)));
-        ARE_CUDA(cudaMalloc(&c.d_part, sizeof(TailPartial) * (size_t)c.grid * K3_GROUP));
-        ARE_CUDA(cudaHostAlloc(&c.h_res, sizeof(double) * 2 * K3_GROUP, cudaHostAllocDefault));
+        ARE_CUDA(cudaMalloc(&c.d_part, sizeof(TailPartial) * (size_t)c.grid * (K3_GROUP + 1)));
+        ARE_CUDA(cudaHostAlloc(&c.h_res, sizeof(double) * (2 * K3_GROUP + 2), cudaHostAllocDefault));
     }
-    for (int64_t base = 0; base < n_rp; base += K3_GROUP) {
+    for (int64_t base = 0; base < std::max<int64_t>(n_rp, summary ? 1 : 0); base += K3_GROUP) {
         K3Params prm{};
         prm.n_rp = (int)std::min<int64_t>(K3_GROUP, n_rp - base);
+        prm.summary = summary && base == 0;
         for (int r = 0; r < prm.n_rp; ++r) {
             int64_t k;
             int rc = order_stat_k(n, rps[base + r], &k);
@@ -394,13 +433,95 @@ int k3_order_stats(const double *d_x, int64_t n, const double *rps, int64_t n_rp
         void *args[] = {(void *)&d_x, (void *)&n, (void *)&prm, (void *)&c.d_work, (void *)&c.d_part};
         ARE_CUDA(cudaLaunchCooperativeKernel((void *)k3_select, grid, K3_THREADS, args, smem, st));
         ARE_LAUNCHED();
-        ARE_CUDA(cudaMemcpyAsync(c.h_res, c.d_work->res, sizeof(double) * 2 * K3_GROUP, cudaMemcpyDeviceToHost, st));
+        ARE_CUDA(cudaMemcpyAsync(c.h_res, c.d_work->res, sizeof(double) * (2 * K3_GROUP + 2), cudaMemcpyDeviceToHost,
+                                 st));
         ARE_CUDA(cudaStreamSynchronize(st));
         for (int r = 0; r < prm.n_rp; ++r) {
             pml_out[base + r] = c.h_res[r];
             tvar_out[base + r] = c.h_res[K3_GROUP + r];
         }
+        if (prm.summary) {
+            summary[0] = c.h_res[2 * K3_GROUP];
+            summary[1] = c.h_res[2 * K3_GROUP + 1];
+        }
     }
+    return ARE_OK;
+}
+
+// ---- many return periods, PML only (ep_curve, metrics.py:97-115) --------
+// The reference sorts the table once for an EP curve (metrics.py:110); so
+// does this: the order-preserving keys (NaN last) are radix-sorted on the
+// device and every requested rank is read from the sorted keys in one
+// gather, where the select kernel would need ceil(n_rp / 8) launches.
+__global__ void k3_keys(const double *__restrict__ x, int64_t n, uint64_t *__restrict__ keys) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = order_key(x[i]);
+}
+__global__ void k3_gather_ranks(const uint64_t *__restrict__ sorted, const int64_t *__restrict__ ranks, int n_rp,
+                                double *__restrict__ out) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rp; r += gridDim.x * blockDim.x)
+        out[r] = key_value(sorted[ranks[r] - 1]);
+}
+
+struct SortCache {
+    std::mutex mu;
+    int64_t cap = 0;         // keys
+    uint64_t *d_keys = nullptr;  // [2 * cap]
+    void *d_tmp = nullptr;
+    size_t tmp_bytes = 0;
+    int64_t rank_cap = 0;
+    int64_t *d_ranks = nullptr;
+    double *d_out = nullptr;
+};
+static SortCache g_sort[64];
+
+int k3_pml_sorted(const double *d_x, int64_t n, const double *rps, int64_t n_rp, double *pml_out, int sms,
+                  cudaStream_t st) {
+    if (n <= 0) return fail(ARE_EINVAL, "empty year loss table");
+    if (n_rp <= 0) return ARE_OK;
+    std::vector<int64_t> ranks((size_t)n_rp);
+    for (int64_t r = 0; r < n_rp; ++r) {
+        int rc = order_stat_k(n, rps[r], &ranks[(size_t)r]);
+        if (rc) return rc;
+    }
+    int dev;
+    ARE_CUDA(cudaGetDevice(&dev));
+    SortCache &c = g_sort[dev & 63];
+    std::lock_guard<std::mutex> guard(c.mu);
+    if (n > c.cap) {
+        cudaFree(c.d_keys);
+        cudaFree(c.d_tmp);
+        c.d_keys = nullptr;
+        c.d_tmp = nullptr;
+        c.cap = 0;
+        size_t tmp = 0;
+        ARE_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, (const uint64_t *)nullptr, (uint64_t *)nullptr, n));
+        ARE_CUDA(cudaMalloc(&c.d_keys, sizeof(uint64_t) * 2 * (size_t)n));
+        ARE_CUDA(cudaMalloc(&c.d_tmp, tmp));
+        c.tmp_bytes = tmp;
+        c.cap = n;
+    }
+    if (n_rp > c.rank_cap) {
+        cudaFree(c.d_ranks);
+        cudaFree(c.d_out);
+        c.d_ranks = nullptr;
+        c.d_out = nullptr;
+        c.rank_cap = 0;
+        ARE_CUDA(cudaMalloc(&c.d_ranks, sizeof(int64_t) * (size_t)n_rp));
+        ARE_CUDA(cudaMalloc(&c.d_out, sizeof(double) * (size_t)n_rp));
+        c.rank_cap = n_rp;
+    }
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+    k3_keys<<<blocks, 256, 0, st>>>(d_x, n, c.d_keys);
+    ARE_LAUNCHED();
+    size_t tmp = c.tmp_bytes;
+    ARE_CUDA(cub::DeviceRadixSort::SortKeys(c.d_tmp, tmp, c.d_keys, c.d_keys + c.cap, n, 0, 64, st));
+    ARE_CUDA(cudaMemcpyAsync(c.d_ranks, ranks.data(), sizeof(int64_t) * (size_t)n_rp, cudaMemcpyHostToDevice, st));
+    k3_gather_ranks<<<(int)std::min<int64_t>((n_rp + 255) / 256, 1024), 256, 0, st>>>(c.d_keys + c.cap, c.d_ranks,
+                                                                                       (int)n_rp, c.d_out);
+    ARE_LAUNCHED();
+    ARE_CUDA(cudaMemcpyAsync(pml_out, c.d_out, sizeof(double) * (size_t)n_rp, cudaMemcpyDeviceToHost, st));
+    ARE_CUDA(cudaStreamSynchronize(st));
     return ARE_OK;
 }
 

@@ -370,7 +370,7 @@ def simulate_layers_device(dyet, pool_tset: TableSet, masks, terms_list, out=Non
     plan = pool_tset.plan(*pool_tset.selection_arrays(None), pool=True)
     st = torch.cuda.current_stream(dyet.device)
     lib = _native.load()
-    flags = variant_flags | (_native.IDS_VALIDATED if dyet.ids_validated else 0)
+    flags = variant_flags | dyet.ids_flag(plan)
     for g in range(0, L, MAX_FUSED_LAYERS):
         m = np.ascontiguousarray(masks[g:g + MAX_FUSED_LAYERS], dtype=np.uint64)
         lt = np.ascontiguousarray([[t.occ_retention, t.occ_limit, t.agg_retention, t.agg_limit]
@@ -385,7 +385,7 @@ def simulate_layers_device(dyet, pool_tset: TableSet, masks, terms_list, out=Non
                 plan.value, m.shape[0], m.ctypes.data, lt.ctypes.data, dyet.d_ids.data_ptr(), dyet._n_ids,
                 dyet.d_offsets.data_ptr(), n, 0, n, out[g].data_ptr(), n, _native.ctypes.c_void_p(st.cuda_stream),
                 flags))
-    if check and not dyet.ids_validated:  # validated ids cannot raise the range flag
+    if check and not flags & _native.IDS_VALIDATED:  # validated ids cannot raise the range flag
         _native.check(lib.are_check_errors(plan.value, _native.ctypes.c_void_p(st.cuda_stream)))
     return out
 

@@ -31,19 +31,28 @@ def _torch():
     return torch
 
 
-_UPLOADER = None
+_UPLOADERS: dict = {}
 
 
-def _uploader():
-    global _UPLOADER
-    if _UPLOADER is None:
+def _uploader(device):
+    """The host->device staging pipeline of `device` (its own stream, events
+    and pinned buffers, created under that device: a copy to another GPU never
+    runs on the first GPU's stream)."""
+    torch = _torch()
+    idx = torch.device(device).index
+    if idx is None:
+        idx = torch.cuda.current_device()
+    up = _UPLOADERS.get(idx)
+    if up is None:
         from .h2d import Uploader
 
         import os
 
-        # the staging copies are host-memory bound: use the cores we have
-        _UPLOADER = Uploader(threads=max(1, min(16, len(os.sched_getaffinity(0)))))
-    return _UPLOADER
+        with torch.cuda.device(idx):
+            # the staging copies are host-memory bound: use the cores we have
+            up = Uploader(threads=max(1, min(16, len(os.sched_getaffinity(0)))))
+        _UPLOADERS[idx] = up
+    return up
 
 
 class _Resident:
@@ -99,12 +108,14 @@ class DeviceYearEventTable:
         self.catalog_size = int(catalog_size)
         self.offsets = np.ascontiguousarray(offsets, dtype=np.int64)
         n = int(self.offsets[-1])
-        # +4 zero ids of padding: 16-byte loads past the last trial stay in bounds
-        self.d_ids = torch.zeros(n + 4, dtype=torch.int32, device=dev)
+        # +4 zero ids of padding: 16-byte loads past the last trial stay in
+        # bounds (only the padding is zeroed; the upload overwrites the rest)
+        self.d_ids = torch.empty(n + 4, dtype=torch.int32, device=dev)
+        self.d_ids[n:].zero_()
         if n:
             src = ids if getattr(ids, "dtype", None) == np.uint32 else np.asarray(ids, dtype=np.uint32)
             with torch.cuda.device(dev):
-                _uploader().copy(self.d_ids[:n], src)
+                _uploader(dev).copy(self.d_ids[:n], src)
         self._n_ids = n
         with warnings.catch_warnings():
             warnings.simplefilter("ignore", UserWarning)  # read-only numpy source
@@ -134,6 +145,16 @@ class DeviceYearEventTable:
                         "ts_min": None, "ts_max": None}
         self.ids_validated = self._n_ids == 0 or rep.max_id <= self.catalog_size
 
+    def ids_flag(self, plan) -> int:
+        """IDS_VALIDATED when every id of this table indexes inside the plan's
+        rows (max id < row_len): a plan over a smaller catalog than the YET's
+        keeps K2's per-id range check."""
+        if not self.ids_validated:
+            return 0
+        if self._n_ids and _native.plan_info(plan).row_len <= int(self._report["max_id"]):
+            return 0
+        return _native.IDS_VALIDATED
+
     def validate_timestamps(self, ts, chunk: int = 1 << 26) -> None:
         """Stream host timestamps through K0 in trial-aligned chunks (kept nowhere)."""
         torch = _torch()
@@ -148,7 +169,7 @@ class DeviceYearEventTable:
             d_ts = torch.empty(max(b - a, 1), dtype=torch.float64, device=self.device)
             if b > a:
                 with torch.cuda.device(self.device):
-                    _uploader().copy(d_ts, np.asarray(ts[a:b], dtype=np.float64))
+                    _uploader(self.device).copy(d_ts, np.asarray(ts[a:b], dtype=np.float64))
             rep = self._k0(d_ts, ts_base=a, t0=t0, t1=t1, ids=False)
             r["unsorted"] += int(rep.unsorted)
             r["ts_nan"] += int(rep.ts_nan)
@@ -205,12 +226,13 @@ class DeviceYearEventTable:
             out = torch.empty(n, dtype=torch.float64, device=self.device)
         st = torch.cuda.current_stream(self.device) if stream is None else stream
         lib = _native.load()
+        flag = self.ids_flag(plan)
         _native.check(lib.are_simulate_device(
             plan.value, self.d_ids.data_ptr(), self._n_ids, self.d_offsets.data_ptr(), n,
             int(first), int(last), float(terms.occ_retention), float(terms.occ_limit),
             float(terms.agg_retention), float(terms.agg_limit), out.data_ptr(),
             ctypes.c_void_p(st.cuda_stream),
-            _native.VARIANTS[variant] | (_native.IDS_VALIDATED if self.ids_validated else 0)))
-        if check and not self.ids_validated:  # validated ids cannot raise the range flag
+            _native.VARIANTS[variant] | flag))
+        if check and not flag:  # validated ids cannot raise the range flag
             _native.check(lib.are_check_errors(plan.value, ctypes.c_void_p(st.cuda_stream)))
         return out

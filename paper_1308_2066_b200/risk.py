@@ -75,6 +75,57 @@ def order_stats(ylt, return_periods: Sequence[float], stream=None) -> tuple[np.n
     return pml_out, tvar_out
 
 
+# Above this many return periods a PML-only request (an EP curve) sorts the
+# table once on the device (are_pml_many_device) instead of running the
+# select kernel once per 8 return periods.
+SORT_MIN_RPS = 9
+
+
+def pml_many(ylt, return_periods: Sequence[float], stream=None) -> np.ndarray:
+    """PML at every return period (no TVaR): one device sort + one gather
+    when there are many, the select kernel otherwise."""
+    src = _source(ylt)
+    n = int(src.shape[0])
+    if n == 0:
+        raise ValueError("empty year loss table")
+    rps = np.ascontiguousarray([float(r) for r in return_periods], dtype=np.float64)
+    for r in rps:
+        _order_stat_k(n, r)
+    if rps.size < SORT_MIN_RPS:
+        return order_stats(src, rps, stream)[0]
+    import torch
+
+    d = src if _is_cuda_tensor(src) else torch.from_numpy(src).cuda()
+    out = np.empty(rps.size)
+    st = torch.cuda.current_stream(d.device) if stream is None else stream
+    with torch.cuda.device(d.device):
+        _native.check(_native.load().are_pml_many_device(d.data_ptr(), n, rps.ctypes.data, rps.size, out.ctypes.data,
+                                                         ctypes.c_void_p(st.cuda_stream)))
+    return out
+
+
+def order_stats_summary(d_ylt, return_periods: Sequence[float], stream=None):
+    """(pml, tvar, mean, max) from one K3 call over a float64 CUDA tensor: the
+    mean and maximum ride along in the tail pass (the pricing service's
+    trial_mean / trial_max, service.py:237-238)."""
+    import torch
+
+    n = int(d_ylt.shape[0])
+    if n == 0:
+        raise ValueError("empty year loss table")
+    rps = np.ascontiguousarray([float(r) for r in return_periods], dtype=np.float64)
+    for r in rps:
+        _order_stat_k(n, r)
+    pml_out = np.empty(max(rps.size, 1))
+    tvar_out = np.empty(max(rps.size, 1))
+    mm = np.empty(2)
+    st = torch.cuda.current_stream(d_ylt.device) if stream is None else stream
+    _native.check(_native.load().are_order_stats_summary_device(
+        d_ylt.data_ptr(), n, rps.ctypes.data, rps.size, pml_out.ctypes.data, tvar_out.ctypes.data, mm.ctypes.data,
+        ctypes.c_void_p(st.cuda_stream)))
+    return pml_out[:rps.size], tvar_out[:rps.size], float(mm[0]), float(mm[1])
+
+
 def pml(ylt, return_period: float) -> float:
     """Probable maximum loss at `return_period` (metrics.py:45-52)."""
     return float(order_stats(ylt, [return_period])[0][0])
@@ -125,7 +176,7 @@ def ep_curve(ylt, return_periods: Iterable[float]) -> EPCurve:
     rps = sorted({float(r) for r in return_periods})
     if not rps:
         raise ValueError("no return periods given")
-    p, _ = order_stats(src, rps)
+    p = pml_many(src, rps)
     return EPCurve(tuple((float(v), 1.0 / rp) for v, rp in zip(p, rps)))
 
 

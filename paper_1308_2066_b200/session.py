@@ -23,7 +23,7 @@ from .direct_access import TableSet
 from .errors import PortfolioInvalidError
 from .portfolio import Layer, LayerTerms, validate_portfolio
 from .resident import DeviceYearEventTable
-from .risk import _order_stat_k, order_stats
+from .risk import _order_stat_k, order_stats_summary, pml_many
 
 DEFAULT_RETURN_PERIODS = (10.0, 50.0, 100.0, 250.0)  # service.py:45
 
@@ -57,16 +57,20 @@ class PricingSession:
         t0 = time.perf_counter()
         self.yet.simulate_device(plan, terms, out=self.d_ylt)
         distinct = sorted(set(rps))
-        p, t = order_stats(self.d_ylt, rps + distinct)
-        mean = float(self.d_ylt.mean())
-        peak = float(self.d_ylt.max())
+        # one K3 call: PML/TVaR, the EP points and the mean/max from its tail
+        # pass (many EP points: one device sort instead)
+        if len(rps) + len(distinct) <= 8:
+            p, t, mean, peak = order_stats_summary(self.d_ylt, rps + distinct)
+            ep = p[len(rps):]
+        else:
+            p, t, mean, peak = order_stats_summary(self.d_ylt, rps)
+            ep = pml_many(self.d_ylt, distinct)
         engine_seconds = time.perf_counter() - t0
         self.reprice_count += 1
-        k = len(rps)
         return {
             "trial_count": n,
             "metrics": [{"return_period": rp, "pml": float(p[i]), "tvar": float(t[i])} for i, rp in enumerate(rps)],
-            "ep_curve": [{"loss": float(p[k + i]), "exceedance_probability": 1.0 / rp}
+            "ep_curve": [{"loss": float(ep[i]), "exceedance_probability": 1.0 / rp}
                          for i, rp in enumerate(distinct)],
             "trial_mean": mean,
             "trial_max": peak,

@@ -12,7 +12,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch  # noqa: E402
 
-from paper_1308_2066_b200.risk import order_stats  # noqa: E402
+import time  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+from paper_1308_2066_b200.risk import ep_curve, order_stats, order_stats_summary, pml_many  # noqa: E402
 
 RPS = [10.0, 50.0, 100.0, 250.0]
 
@@ -45,5 +49,24 @@ def main() -> None:
                           "pml": list(pml), "tvar": list(tvar)}))
 
 
+def ep_timing(n: int) -> None:
+    """A 100-point EP curve: one sort (pml_many) vs the select kernel in
+    groups of 8 (order_stats), wall per call (both synchronise)."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.rand(n, generator=g, device="cuda", dtype=torch.float64) * 1e5
+    rps = list(np.geomspace(1.01, n, 100))
+    for name, fn in [("ep100_sort", lambda: pml_many(x, rps)), ("ep100_select", lambda: order_stats(x, rps)),
+                     ("ep_curve_100", lambda: ep_curve(x, rps)),
+                     ("summary_4rp_mean_max", lambda: order_stats_summary(x, RPS))]:
+        for _ in range(3):
+            fn()
+        reps = 20
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        print(json.dumps({"case": name, "n": n, "us_per_call_wall": (time.perf_counter() - t0) * 1e6 / reps}))
+
+
 if __name__ == "__main__":
     main()
+    ep_timing(int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000)

@@ -122,3 +122,37 @@ def test_k3_edge_cases(case, rng):
         assert _same(pv, oracle.pml(x, r)), (r, pv, oracle.pml(x, r))
         want = oracle.tvar(x, r)
         assert (np.isnan(tv) and np.isnan(want)) or tv == pytest.approx(want, rel=1e-12, abs=1e-300)
+
+
+def test_ep_curve_many_points_one_sort(rng):
+    """Many return periods: one device sort of the keys (are_pml_many_device)
+    -- the reference's own one-sort EP curve (metrics.py:97-115) -- exact
+    points, including ties at a cap, negative zero and NaN (sorted last)."""
+    import torch
+
+    x = np.minimum(rng.lognormal(8.0, 2.0, 1_000_000), 66_000.0)
+    x[rng.integers(0, x.size, 1000)] = 0.0
+    x[:3] = [-0.0, np.nan, 1e300]
+    rps = np.unique(np.concatenate([np.geomspace(1.01, 1e6, 97), [2.0, 10.0, 1e6]]))
+    want = oracle.ep_points(x, rps)
+    assert len(want) == rps.size and not any(np.isnan(a) for a, _ in want)  # NaN sorts past every rank asked
+    got = ep_curve(YearLossTable("x", x), rps)
+    assert list(got.points) == list(want)
+    assert np.signbit(got.points[0][0]) == np.signbit(want[0][0])
+    assert list(ep_curve(torch.from_numpy(x).cuda(), rps).points) == list(want)
+
+
+def test_summary_mean_and_max_ride_in_k3(rng):
+    import torch
+
+    from paper_1308_2066_b200.risk import order_stats_summary
+
+    x = rng.lognormal(6.0, 1.5, 300_001)
+    p, t, mean, peak = order_stats_summary(torch.from_numpy(x).cuda(), [10.0, 100.0])
+    assert list(p) == [oracle.pml(x, 10.0), oracle.pml(x, 100.0)]
+    assert t[1] == pytest.approx(oracle.tvar(x, 100.0), rel=1e-12)
+    assert peak == x.max() and mean == pytest.approx(x.mean(), rel=1e-13)
+    y = x.copy()
+    y[5] = np.nan
+    _, _, mean, peak = order_stats_summary(torch.from_numpy(y).cuda(), [10.0])
+    assert np.isnan(mean) and np.isnan(peak)
