@@ -383,6 +383,7 @@ static void fill_args(const are_plan_s *p, K2Args &a, double occ_ret, double occ
     a.rnbits = (uint32_t)p->rnbits;
     a.rhash_mode = p->rhash_mode;
     a.rsmem = p->rsmem;
+    a.rtex = p->rb.tex;
 }
 
 // K2 over trials [first, last) of ids/offsets indexed from id_base/t_base

@@ -210,6 +210,19 @@ int k1_build_relay(const PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int
         ARE_LAUNCHED();
     }
     rb.filter_words = (filter_bits + 31) / 32;  // the per-terms filters (k1_relay_filter)
+    if (row_len * 2 <= (int64_t)1 << 27) {  // linear textures hold up to 2^27 texels
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypeLinear;
+        rd.res.linear.devPtr = rb.rslots;
+        rd.res.linear.desc = cudaCreateChannelDesc(32, 32, 32, 32, cudaChannelFormatKindUnsigned);
+        rd.res.linear.sizeInBytes = (size_t)row_len * sizeof(RSlot);
+        cudaTextureDesc td{};
+        td.readMode = cudaReadModeElementType;
+        if (cudaCreateTextureObject(&rb.tex, &rd, &td, nullptr) != cudaSuccess) {
+            cudaGetLastError();
+            rb.tex = 0;
+        }
+    }
     return ARE_OK;
 }
 

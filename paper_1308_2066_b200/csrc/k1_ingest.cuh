@@ -18,7 +18,10 @@ struct RelayBuffers {
     RSlot *rslots = nullptr;     // row_len records
     double *rovf = nullptr;      // fin-applied overflow values (same indexing as PlanBuffers::ovf)
     int64_t filter_words = 0;    // words of each per-terms filter (k1_relay_filter)
+    cudaTextureObject_t tex = 0; // rslots as uint4 texels (gathers through the texture pipe)
     void release() {
+        if (tex) cudaDestroyTextureObject(tex);
+        tex = 0;
         cudaFree(rslots);
         cudaFree(rovf);
         rslots = nullptr;

@@ -46,11 +46,11 @@ namespace are {
 #ifndef ARE_KR_ROWDRAIN
 #define ARE_KR_ROWDRAIN 0  // drain the queue after every row (64-entry queue) instead of every two
 #endif
+#ifndef ARE_KR_TEX
+#define ARE_KR_TEX 1       // gather the records through the texture pipe (tex1Dfetch): off the LSU pipe the kernel is bound by
+#endif
 #ifndef ARE_KR_EXP
 #define ARE_KR_EXP 0       // timing experiments only (results are wrong when != 0)
-#endif
-#ifndef ARE_KR_PF
-#define ARE_KR_PF 0        // L2 bulk prefetch of ids: 0 = none (measured best), 1 = chunks ch+4..ch+6 every 3 chunks, 2 = the next trial at trial start
 #endif
 static constexpr int KR_NF = ARE_KR_NF;
 static constexpr int KR_NP = (K2R_THREADS / 32 - KR_NF) / KR_NF * KR_NF;  // producer warps
@@ -235,58 +235,57 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
             return RRaw{__hiloint2double((int)r.y, (int)r.x), 0.0, 0.0, __hiloint2double((int)r.w, (int)r.z)};
         }
 #endif
+#if ARE_KR_TEX
+        // through the texture pipe (the host runs this kernel only with a
+        // texture object over the records)
+        const int i = (int)(2u * ((uint32_t)lane < n ? e : 0u));
+        RRaw r;
+        asm volatile("{\n\t.reg .b32 a0, a1, a2, a3, b0, b1, b2, b3;\n\t"
+                     "tex.1d.v4.u32.s32 {a0, a1, a2, a3}, [%4, {%5}];\n\t"
+                     "tex.1d.v4.u32.s32 {b0, b1, b2, b3}, [%4, {%6}];\n\t"
+                     "mov.b64 %0, {a0, a1};\n\tmov.b64 %1, {a2, a3};\n\t"
+                     "mov.b64 %2, {b0, b1};\n\tmov.b64 %3, {b2, b3};\n\t}"
+                     : "=d"(r.x0), "=d"(r.f1), "=d"(r.f2), "=d"(r.m)
+                     : "l"(a.rtex), "r"(i), "r"(i + 1));
+        return r;
+#else
         return ld_rslot(a.rslots + ((uint32_t)lane < n ? e : 0u), pol_keep);
+#endif
     };
 
+    // A trial's ids are streamed as 128-id chunks aligned to 128-byte lines
+    // (`skew` positions before the trial; `rel` wraps below zero there, so one
+    // unsigned compare bounds both ends).  The next trial's first two chunks
+    // are requested before the current trial's final batch is flushed, so
+    // their latency overlaps that batch's gather.
     int64_t t = a.first + (int64_t)blockIdx.x * KR_NP + warp;
-    int64_t lo = 0, hi = 0;
-    if (t < a.last) {
-        lo = a.offsets[t - a.t_base];
-        hi = a.offsets[t - a.t_base + 1];
-    }
-#if ARE_KR_PF == 2
-    int64_t nlo = 0, nhi = 0;  // the next trial's bounds: known one trial ahead
-    if (t + W < a.last) {
-        nlo = a.offsets[t + W - a.t_base];
-        nhi = a.offsets[t + W - a.t_base + 1];
-    }
-#endif
-    for (; t < a.last; t += W) {
-#if ARE_KR_PF == 2
-        const int64_t tnn = t + 2 * W;
-        int64_t nnlo = 0, nnhi = 0;
-        if (tnn < a.last) {  // bounds two trials ahead, in flight during this trial
-            nnlo = a.offsets[tnn - a.t_base];
-            nnhi = a.offsets[tnn - a.t_base + 1];
-        }
-        if (lane == 0 && nhi > nlo) {  // the next trial's ids to L2 (16-byte aligned span)
-            const uintptr_t b0 = reinterpret_cast<uintptr_t>(ids + (nlo - a.id_base)) & ~(uintptr_t)15;
-            const uintptr_t b1 = (reinterpret_cast<uintptr_t>(ids + (nhi - a.id_base)) + 15) & ~(uintptr_t)15;
-            prefetch_l2_bulk(reinterpret_cast<const void *>(b0), (uint32_t)(b1 - b0));
-        }
-#else
-        const int64_t tn = t + W;
-        int64_t nlo = 0, nhi = 0;
-        if (tn < a.last) {  // next trial's bounds, in flight during this trial
-            nlo = a.offsets[tn - a.t_base];
-            nhi = a.offsets[tn - a.t_base + 1];
-        }
-#endif
+    uint32_t len = 0, rel = 0;
+    const uint32_t *p = ids;
+    int nchunks = 0;
+    uint32_t r0[4], r1[4], r2[4];
+    int64_t nlo = 0, nhi = 0;  // the bounds of the warp's next trial
+    auto begin = [&](int64_t lo, int64_t hi) {
         const int64_t rlo = lo - a.id_base;
-        const uint32_t len = (uint32_t)(hi - lo);
+        len = (uint32_t)(hi - lo);
         const uint32_t skew = (uint32_t)((reinterpret_cast<uintptr_t>(ids + rlo) >> 2) & 31);
-        const uint32_t *p = ids + (rlo - skew) + lane;
-        uint32_t rel = (uint32_t)lane - skew;
-        const int nchunks = (int)((len + skew + 127) >> 7);
-        uint32_t qh = 0, qt = 0;
-        bool pending = false;
-        RRaw ps{0.0, 0.0, 0.0, 0.0};
-
-        uint32_t r0[4], r1[4], r2[4];
+        p = ids + (rlo - skew) + lane;
+        rel = (uint32_t)lane - skew;
+        nchunks = (int)((len + skew + 127) >> 7);
 #pragma unroll
         for (int k = 0; k < 4; ++k) r0[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream, pad);
 #pragma unroll
         for (int k = 0; k < 4; ++k) r1[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream, pad);
+    };
+    if (t < a.last) begin(a.offsets[t - a.t_base], a.offsets[t - a.t_base + 1]);
+    for (; t < a.last; t += W) {
+        const int64_t tn = t + W;
+        if (tn < a.last) {  // next trial's bounds, in flight during this trial
+            nlo = a.offsets[tn - a.t_base];
+            nhi = a.offsets[tn - a.t_base + 1];
+        }
+        uint32_t qh = 0, qt = 0;
+        bool pending = false;
+        RRaw ps{0.0, 0.0, 0.0, 0.0};
 
         auto step = [&](uint32_t (&cur)[4], uint32_t (&fut)[4]) {
             const uint32_t rel0 = rel - (uint32_t)lane + 256u;  // start of the chunk loaded now, trial-relative
@@ -348,18 +347,13 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
             rel += 128;
         };
         for (int ch = 0; ch < nchunks; ch += 3) {
-#if ARE_KR_PF == 1
-            if (lane == 0) {  // chunks ch+4 .. ch+6 to L2 ahead of their row loads
-                const uint32_t a0 = rel - (uint32_t)lane + 512u;
-                if ((int32_t)a0 < (int32_t)len) prefetch_l2_bulk(p - lane + 512, 1536);
-            }
-#endif
             step(r0, r2);
             if (ch + 1 >= nchunks) break;
             step(r1, r0);
             if (ch + 2 >= nchunks) break;
             step(r2, r1);
         }
+        if (tn < a.last) begin(nlo, nhi);  // the next trial's first chunks, in flight during the flush
         const uint32_t n = qt - qh;  // final partial batch
         const double v = value(ps);
         if (n) {
@@ -369,12 +363,6 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
         } else {
             push(pending ? v : 0.0, 1u);
         }
-        lo = nlo;
-        hi = nhi;
-#if ARE_KR_PF == 2
-        nlo = nnlo;
-        nhi = nnhi;
-#endif
     }
 #if ARE_KR_EXP
     if (emax == 0xFFFFFFFFu) a.out[0] = 1.0;

@@ -830,7 +830,7 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
     if (g > sms) g = sms;  // persistent: one CTA per SM (the filter fills shared memory)
     const dim3 grid((unsigned)g), block(K2_THREADS);
     const int sel = a.hash_mode * 2 + (check ? 1 : 0);
-    if (a.rslots && !a.precombined && !use_pair(a.mean_len)) {
+    if (a.rslots && a.rtex && !a.precombined && !use_pair(a.mean_len)) {
         // the relay kernel, over its own filter
         K2Args b = a;
         b.filter = a.rfilter;

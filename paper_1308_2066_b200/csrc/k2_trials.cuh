@@ -49,6 +49,7 @@ struct K2Args {
     uint32_t rnbits = 0;
     int32_t rhash_mode = 0;
     size_t rsmem = 0;
+    unsigned long long rtex = 0;  // texture object over rslots (uint4 texels), 0: none
 };
 
 // Threads per CTA of the hot-set kernel (one persistent CTA per SM).
