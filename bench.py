@@ -97,11 +97,12 @@ def _peaks() -> tuple[float, str]:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def _traffic() -> float | None:
-    """DRAM bytes per K2 launch from the committed ncu capture, if any."""
+def _traffic(kernel: str) -> float | None:
+    """DRAM bytes per K2 launch from the committed ncu capture of `kernel`, if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "k2_traffic.json")) as f:
-            return float(json.load(f)["dram_bytes_per_launch"])
+            d = json.load(f)
+        return float(d["dram_bytes_per_launch"]) if d.get("kernel", "k2_hotset") == kernel else None
     except Exception:
         return None
 
@@ -341,7 +342,7 @@ def roofline(trials: int, kernel_ms: float, kernel: str) -> dict:
     peak, peak_src = _peaks()
     hbm = trials * compulsory_bytes_per_trial()
     achieved = hbm / (kernel_ms / 1e3) / 1e9
-    traffic = _traffic() if kernel == "k2_hotset" else None  # the committed capture is of k2_hotset
+    traffic = _traffic(kernel)
     lk = trials * bytes_per_trial()
     return {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -502,6 +503,9 @@ def run_ours(args) -> None:
         step()
     _native.check(_native.load().are_check_errors(plan.value, None))
     torch.cuda.synchronize(dev)
+    if workload != "c3":
+        info = _native.plan_info(plan)  # the relay records are built by the first launch
+        kernel_name = "k2_relay" if info.relay else "k2_hotset"
     if world > 1:
         dist.barrier()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
@@ -685,7 +689,8 @@ def run_ours(args) -> None:
         "clocks": clocks.summary(),
         "hot_set": {"hot_events": info.hot_events, "entries": info.entries,
                     "overflow_entries": info.overflow_entries, "filter_bits": info.filter_bits,
-                    "smem_bytes": info.smem_bytes},
+                    "smem_bytes": info.smem_bytes, "relay": bool(info.relay),
+                    "relay_filter_bits": info.relay_filter_bits, "relay_smem_bytes": info.relay_smem_bytes},
         **side,
         "pml": list(map(float, pml_v)), "tvar": list(map(float, tvar_v)),
         "setup_seconds": {"generate": gen_s},

@@ -69,6 +69,9 @@ typedef struct {
     int64_t device_bytes;     /* device memory owned by the plan                  */
     int32_t zero_skip_exact;  /* every fin_j(+-0) == +-0 (hot-set kernel usable)  */
     int32_t smem_bytes;       /* dynamic shared memory of the hot-set kernel      */
+    int64_t relay_filter_bits; /* bits of the relay kernel's per-terms filter (0: no relay records yet) */
+    int32_t relay;            /* 1 when long-trial launches run k2_relay (records built on first use) */
+    int32_t relay_smem_bytes; /* dynamic shared memory of k2_relay               */
 } are_plan_info_t;
 
 /* ---- library / device ------------------------------------------------ */

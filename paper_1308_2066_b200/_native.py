@@ -54,6 +54,9 @@ class PlanInfo(ctypes.Structure):
         ("device_bytes", _I64),
         ("zero_skip_exact", _I32),
         ("smem_bytes", _I32),
+        ("relay_filter_bits", _I64),
+        ("relay", _I32),
+        ("relay_smem_bytes", _I32),
     ]
 
 

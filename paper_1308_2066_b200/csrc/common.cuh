@@ -53,16 +53,29 @@ struct __align__(16) Entry {
     uint32_t pad;
 };
 
-// Relay-kernel record (k2_relay.cu), one per event id, 32 bytes (one 256-bit
-// load): the event's selected entries with the financial terms already
-// applied by K1 -- x0 = 0.0 + f_{j1}(x_{j1}) (the first partial sum of comb),
-// f1/f2 the 2nd/3rd entries' f_j(x_j), cnt the number of non-zero entries,
-// ovf the index in the relay overflow array of the 4th entry.
-struct __align__(32) RSlot {
-    double x0, f1, f2;
-    uint32_t cnt;
-    uint32_t ovf;
+// Relay-kernel record (k2_relay.cu), one per event id, 16 bytes (one
+// texture texel): the event's selected entries with the financial terms
+// already applied by K1, f_j(x_j) = share_j * clamp(rate_j * x_j - ret_j, 0,
+// lim_j) in selection order j1 < j2 < ...
+//   simple event (at most 2 entries, none NaN):
+//       a = 0.0 + f_{j1}   (the first partial sum of comb; +0.0 when absent)
+//       b = f_{j2}, or +0.0 when the event has one entry or none
+//     comb = a + b is then exactly the reference's sum: for one entry the
+//     extra +0.0 leaves a (never -0.0, being 0.0 + f) unchanged;
+//   complex event (3+ entries, or a NaN among the first two):
+//       a = a quiet NaN whose payload holds cnt (bits 32..50) and the index
+//           in the relay overflow array of entry 2 (bits 0..31)
+//       b = 0.0 + f_{j1}
+//     comb = b + ovf[i] + ovf[i + 1] + ... (cnt - 1 overflow entries).
+struct __align__(16) RSlot {
+    double a, b;
 };
+static constexpr unsigned long long RSLOT_COMPLEX = 0x7FF8000000000000ull;  // the NaN tag of a complex record
+__device__ __forceinline__ bool rslot_complex(double a) { return a != a; }
+__device__ __forceinline__ uint32_t rslot_cnt(double a) {
+    return (uint32_t)((unsigned long long)__double_as_longlong(a) >> 32) & 0x7FFFFu;
+}
+__device__ __forceinline__ uint32_t rslot_ovf(double a) { return (uint32_t)__double2loint(a); }
 
 // Financial terms of one selected table (FinancialTerms, model.py:46-66).
 struct __align__(32) Fin {

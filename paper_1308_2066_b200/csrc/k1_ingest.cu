@@ -167,22 +167,30 @@ __global__ void k1_relay_slots(const Slot *__restrict__ slots, const Entry *__re
         const Slot s = slots[e];
         const uint32_t cnt = s.meta >> 16;
         RSlot r;
-        r.x0 = 0.0;
-        r.f1 = 0.0;
-        r.f2 = 0.0;
-        r.cnt = cnt;
-        r.ovf = cnt >= 4 ? s.ovf + 2 : 0;
-        if (cnt) r.x0 = __dadd_rn(0.0, fin_term(fin[s.meta & 0xFFFFu], s.x));
-        if (cnt >= 2) {
-            const Entry en = ovf[s.ovf];
-            r.f1 = fin_term(fin[en.j], en.x);
-        }
-        if (cnt >= 3) {
-            const Entry en = ovf[s.ovf + 1];
-            r.f2 = fin_term(fin[en.j], en.x);
+        r.a = 0.0;
+        r.b = 0.0;
+        if (cnt) {
+            const double x0 = __dadd_rn(0.0, fin_term(fin[s.meta & 0xFFFFu], s.x));
+            const double f1 = cnt >= 2 ? fin_term(fin[ovf[s.ovf].j], ovf[s.ovf].x) : 0.0;
+            if (cnt <= 2 && !(x0 != x0) && !(f1 != f1)) {
+                r.a = x0;
+                r.b = f1;
+            } else {  // complex: entries 2..cnt from the relay overflow array
+                r.a = __longlong_as_double((long long)(RSLOT_COMPLEX | ((unsigned long long)cnt << 32) | s.ovf));
+                r.b = x0;
+            }
         }
         rs[e] = r;
     }
+}
+
+// comb of one relay record, in the reference's order (K2 and the filter)
+__device__ __forceinline__ double relay_comb(const RSlot &r, const double *__restrict__ rovf) {
+    if (!rslot_complex(r.a)) return __dadd_rn(r.a, r.b);
+    double comb = r.b;
+    const uint32_t cnt = rslot_cnt(r.a), o = rslot_ovf(r.a);
+    for (uint32_t i = 1; i < cnt; ++i) comb = __dadd_rn(comb, rovf[o + i - 1]);
+    return comb;
 }
 
 __global__ void k1_relay_ovf(const Entry *__restrict__ ovf, const Fin *__restrict__ fin, int64_t n,
@@ -210,7 +218,7 @@ int k1_build_relay(const PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int
         ARE_LAUNCHED();
     }
     rb.filter_words = (filter_bits + 31) / 32;  // the per-terms filters (k1_relay_filter)
-    if (row_len * 2 <= (int64_t)1 << 27) {  // linear textures hold up to 2^27 texels
+    if (row_len <= (int64_t)1 << 27) {  // linear textures hold up to 2^27 texels
         cudaResourceDesc rd{};
         rd.resType = cudaResourceTypeLinear;
         rd.res.linear.devPtr = rb.rslots;
@@ -243,11 +251,8 @@ __global__ void k1_relay_filter_kernel(const RSlot *__restrict__ rs, const doubl
         if (b < nbits)
             for (int64_t e = b; e < row_len; e += nbits) {
                 const RSlot r = rs[e];
-                if (!r.cnt) continue;
-                double comb = r.x0;
-                if (r.cnt >= 2) comb = __dadd_rn(comb, r.f1);
-                if (r.cnt >= 3) comb = __dadd_rn(comb, r.f2);
-                for (uint32_t i = 3; i < r.cnt; ++i) comb = __dadd_rn(comb, rovf[r.ovf + i - 3]);
+                if (!__double_as_longlong(r.a) && !__double_as_longlong(r.b)) continue;  // comb = +0.0
+                const double comb = relay_comb(r, rovf);
                 double v = __dsub_rn(comb, occ_ret);
                 if (v < 0.0) v = 0.0;
                 if (v > occ_lim) v = occ_lim;

@@ -18,10 +18,12 @@
 //     ...: they stream the trial's ids (32-id coalesced rows, two 128-id
 //     chunks in flight), test each id against the shared-memory filter,
 //     append the hot ones in trial order to a per-warp queue, and per 32
-//     queued events gather one 32-byte record per lane (one 256-bit L2 load:
-//     the event's first partial sum, its 2nd and 3rd entries, the count) and
-//     compute the event's occurrence value.  The 32 values go to the warp's
-//     ring in shared memory -- one STS per lane -- instead of being folded;
+//     queued events gather one 16-byte record per lane (one texture texel:
+//     the event's first partial sum and its second entry, or a tagged
+//     pointer to its entries for the rare events with 3+; common.cuh RSlot)
+//     and compute the event's occurrence value.  The 32 values go to the
+//     warp's ring in shared memory -- one STS per lane -- instead of being
+//     folded;
 //   * warp 31 ("fold") folds: lane l consumes producer l's ring, adding each
 //     batch's 32 values to its trial's running sum strictly in order (+0.0 for
 //     lanes past a trial's last event: c >= +0, so that is exact), and writes
@@ -49,6 +51,9 @@ namespace are {
 #ifndef ARE_KR_TEX
 #define ARE_KR_TEX 1       // gather the records through the texture pipe (tex1Dfetch): off the LSU pipe the kernel is bound by
 #endif
+#ifndef ARE_KR_TMAF
+#define ARE_KR_TMAF 1      // the filter enters shared memory by TMA bulk copies (one thread, no register staging)
+#endif
 #ifndef ARE_KR_EXP
 #define ARE_KR_EXP 0       // timing experiments only (results are wrong when != 0)
 #endif
@@ -61,20 +66,21 @@ static constexpr int KR_RSTRIDE = KR_NB * 32 + 2;  // doubles per ring (+16 B: t
 
 size_t k2_relay_fixed_smem() {
     return (size_t)KR_NP * KR_QCAP * sizeof(uint32_t) + (size_t)KR_NP * KR_RSTRIDE * sizeof(double) +
-           (size_t)2 * 32 * KR_NB * sizeof(uint64_t) + (size_t)32 * KR_NB * sizeof(uint32_t);
+           (size_t)2 * 32 * KR_NB * sizeof(uint64_t) + (size_t)32 * KR_NB * sizeof(uint32_t) + 16;
 }
 
 // A gathered relay record kept exactly as loaded (four doubles; count and
 // overflow index decoded where used), so the loop-carried pending batch can
 // live in the load's own destination registers (no copy of an in-flight load).
+// A gathered relay record kept exactly as loaded (RSlot's two doubles,
+// decoded where the value is computed, one batch later), so the loop-carried
+// pending batch lives in the load's own destination registers.
 struct RRaw {
-    double x0, f1, f2, m;
+    double a, b;
 };
 __device__ __forceinline__ RRaw ld_rslot(const RSlot *p, uint64_t policy) {
     RRaw r;
-    asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=d"(r.x0), "=d"(r.f1), "=d"(r.f2), "=d"(r.m)
-                 : "l"(p), "l"(policy));
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(r.a), "=d"(r.b) : "l"(p), "l"(policy));
     return r;
 }
 // mbarrier helpers (shared::cta).  arrive has release and test/try_wait
@@ -170,16 +176,38 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
     const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(s_bar);
     const uint32_t empty0 = full0 + 32 * KR_NB * 8;
     {
+#if ARE_KR_TMAF
+        // one thread hands the whole filter to the TMA unit in 16 KB bulk
+        // copies completing on one mbarrier (no LDG/STS round trips through
+        // registers)
+        const uint32_t fbar = (uint32_t)__cvta_generic_to_shared(s_end + 32 * KR_NB);
+        if (threadIdx.x == 0) {
+            const uint32_t bytes = a.filter_words * 4u, dst = (uint32_t)__cvta_generic_to_shared(s_filter);
+            mbar_init(fbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fbar), "r"(bytes) : "memory");
+            for (uint32_t off = 0; off < bytes; off += 16384u) {
+                const uint32_t n = min(16384u, bytes - off);
+                asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + off),
+                             "l"(reinterpret_cast<const unsigned char *>(a.filter) + off), "r"(n), "r"(fbar)
+                             : "memory");
+            }
+        }
+#else
         const uint4 *src = reinterpret_cast<const uint4 *>(a.filter);
         uint4 *dst = reinterpret_cast<uint4 *>(s_filter);
         const int n4 = (int)(a.filter_words >> 2);
         for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+#endif
         if (threadIdx.x < KR_NP * KR_NB) {
             mbar_init(full0 + threadIdx.x * 8, 32);  // the producer's 32 lanes
             mbar_init(empty0 + threadIdx.x * 8, 1);  // its fold lane
         }
     }
     __syncthreads();
+#if ARE_KR_TMAF
+    mbar_wait((uint32_t)__cvta_generic_to_shared(s_end + 32 * KR_NB), 0);
+#endif
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (warp >= KR_NP) {
@@ -214,14 +242,14 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
     // occurrence value of this lane's gathered event (slot 0 -- empty -- for
     // lanes past the batch: comb = +0.0, v = clamp(-occ_ret) = +-0)
     auto value = [&](const RRaw &s) -> double {
-        const uint32_t cnt = (uint32_t)__double2loint(s.m);
-        double comb = s.x0;
-        if (cnt >= 2u) comb = __dadd_rn(comb, s.f1);
-        if (cnt >= 3u) {
-            comb = __dadd_rn(comb, s.f2);
-            const uint32_t ovf = (uint32_t)__double2hiint(s.m);
+        double comb;
+        if (!rslot_complex(s.a)) {
+            comb = __dadd_rn(s.a, s.b);  // one or two entries (RSlot)
+        } else {
+            comb = s.b;
+            const uint32_t cnt = rslot_cnt(s.a), o = rslot_ovf(s.a);
 #pragma unroll 1
-            for (uint32_t i = 3; i < cnt; ++i) comb = __dadd_rn(comb, a.rovf[ovf + i - 3]);
+            for (uint32_t i = 1; i < cnt; ++i) comb = __dadd_rn(comb, a.rovf[o + i - 1]);
         }
         return clamp_ref(__dsub_rn(comb, occ_ret), occ_lim);
     };
@@ -229,24 +257,17 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
         const uint32_t e = q[(qh + lane) & (KR_QCAP - 1)];
 #if ARE_KR_EXP == 4  // timing experiment: every gather from a 512 KB window
         return ld_rslot(a.rslots + ((uint32_t)lane < n ? (e & 0x3FFFu) : 0u), pol_keep);
-#elif ARE_KR_EXP == 5  // timing experiment: 16-byte gathers of the same records
-        {
-            const uint4 r = ld_stream_u4(reinterpret_cast<const uint32_t *>(a.rslots + ((uint32_t)lane < n ? e : 0u)), pol_keep);
-            return RRaw{__hiloint2double((int)r.y, (int)r.x), 0.0, 0.0, __hiloint2double((int)r.w, (int)r.z)};
-        }
 #endif
 #if ARE_KR_TEX
         // through the texture pipe (the host runs this kernel only with a
-        // texture object over the records)
-        const int i = (int)(2u * ((uint32_t)lane < n ? e : 0u));
+        // texture object over the records): one 16-byte texel per record
+        const int i = (int)((uint32_t)lane < n ? e : 0u);
         RRaw r;
-        asm volatile("{\n\t.reg .b32 a0, a1, a2, a3, b0, b1, b2, b3;\n\t"
-                     "tex.1d.v4.u32.s32 {a0, a1, a2, a3}, [%4, {%5}];\n\t"
-                     "tex.1d.v4.u32.s32 {b0, b1, b2, b3}, [%4, {%6}];\n\t"
-                     "mov.b64 %0, {a0, a1};\n\tmov.b64 %1, {a2, a3};\n\t"
-                     "mov.b64 %2, {b0, b1};\n\tmov.b64 %3, {b2, b3};\n\t}"
-                     : "=d"(r.x0), "=d"(r.f1), "=d"(r.f2), "=d"(r.m)
-                     : "l"(a.rtex), "r"(i), "r"(i + 1));
+        asm volatile("{\n\t.reg .b32 a0, a1, a2, a3;\n\t"
+                     "tex.1d.v4.u32.s32 {a0, a1, a2, a3}, [%2, {%3}];\n\t"
+                     "mov.b64 %0, {a0, a1};\n\tmov.b64 %1, {a2, a3};\n\t}"
+                     : "=d"(r.a), "=d"(r.b)
+                     : "l"(a.rtex), "r"(i));
         return r;
 #else
         return ld_rslot(a.rslots + ((uint32_t)lane < n ? e : 0u), pol_keep);
@@ -285,7 +306,7 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
         }
         uint32_t qh = 0, qt = 0;
         bool pending = false;
-        RRaw ps{0.0, 0.0, 0.0, 0.0};
+        RRaw ps{};
 
         auto step = [&](uint32_t (&cur)[4], uint32_t (&fut)[4]) {
             const uint32_t rel0 = rel - (uint32_t)lane + 256u;  // start of the chunk loaded now, trial-relative
@@ -330,6 +351,22 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
                     // the pending batch's value first, then the new gather into
                     // the same registers: no register copy of an in-flight load
                     const double v = value(ps);
+#if ARE_KR_EXP == 5  // timing experiment: gather, no value, no push
+                    emax ^= (uint32_t)__double2loint(ps.a) ^ (uint32_t)__double2hiint(ps.b);
+                    ps = gather(qh, 32u);
+                    qh += 32u;
+                    continue;
+#endif
+#if ARE_KR_EXP == 6  // timing experiment: value of the queued ids (no gather), no push
+                    {
+                        const double v6 = value(ps);
+                        if (v6 == 12345.0) emax++;
+                        const uint32_t e6 = q[(qh + lane) & (KR_QCAP - 1)];
+                        ps = RRaw{(double)e6, 0.0};
+                        qh += 32u;
+                        continue;
+                    }
+#endif
 #if ARE_KR_EXP == 3  // timing experiment: no push
                     ps = gather(qh, 32u);
                     if (v == 12345.0) emax++;

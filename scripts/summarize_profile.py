@@ -115,8 +115,10 @@ def main() -> None:
         f.write("\n".join(lines) + "\n")
     if args.traffic_json:
         with open(args.traffic_json, "w") as f:
+            name = m["Kernel Name"][0] if "Kernel Name" in m else ""
+            kernel = next((k for k in ("k2_relay", "k2_hotset", "k2_pair", "k2_dense") if k in name), name)
             json.dump({"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-                       "duration_s": dur, "report": args.rep}, f, indent=1)
+                       "duration_s": dur, "report": args.rep, "kernel": kernel}, f, indent=1)
     print("\n".join(lines[:14]))
 
 

@@ -83,3 +83,31 @@ def test_kernel_paths_agree_bitwise(case):
     hot, _ = price_layer(yet, tset, None, terms)
     dense, _ = price_layer(yet, tset, None, terms, EngineConfig(variant="dense"))
     assert hot.tobytes() == dense.tobytes() == _oracle(yet, stacked, fin, terms).tobytes()
+
+
+def test_ragged_trials_across_the_stream(case):
+    """The relay warps stream their trials back to back (a trial's first ids
+    are loaded while the previous trial is still filtered; a trial's final
+    batch is published with the next push).  Mix empty trials, single-id
+    trials, trials of exactly 31/32/33/128/129 ids and long ones (mean length
+    stays above the short-trial kernel's range), under terms where every,
+    some and no hot event contributes."""
+    yet, elts, tset, stacked, fin = case
+    from paper_1308_2066_b200.portfolio import YearEventTable
+
+    rng = np.random.default_rng(2066)
+    pattern = [0, 1, 0, 0, 31, 32, 33, 128, 129, 1500, 0, 2, 700, 3000, 0, 5, 257, 1, 0, 4096]
+    lengths = np.array([pattern[i % len(pattern)] for i in range(9_001)], dtype=np.int64)
+    rng.shuffle(lengths[: len(lengths) // 2])
+    offsets = np.zeros(lengths.size + 1, dtype=np.int64)
+    np.cumsum(lengths, out=offsets[1:])
+    assert offsets[-1] / lengths.size > 320  # the relay kernel's range
+    src = yet.event_ids
+    ids = src[rng.integers(0, src.size, size=int(offsets[-1]))]
+    ragged = YearEventTable(yet.catalog_size, ids, None, offsets)
+    for occ_ret, occ_lim in [(0.0, math.inf), (500.0, 10_000.0), (9_000.0, 1.0), (1e12, math.inf)]:
+        terms = LayerTerms(occ_ret, occ_lim, 1_000.0, 2e6)
+        got, lookups = price_layer(ragged, tset, None, terms)
+        want = _oracle(ragged, stacked, fin, terms)
+        assert got.tobytes() == want.tobytes(), (occ_ret, occ_lim)
+        assert lookups == len(elts) * ids.size
