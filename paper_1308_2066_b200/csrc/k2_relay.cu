@@ -54,6 +54,9 @@ namespace are {
 #ifndef ARE_KR_TMAF
 #define ARE_KR_TMAF 1      // the filter enters shared memory by TMA bulk copies (one thread, no register staging)
 #endif
+#ifndef ARE_KR_NOALLOC
+#define ARE_KR_NOALLOC 0   // record gathers (load path) bypass L1 allocation
+#endif
 #ifndef ARE_KR_EXP
 #define ARE_KR_EXP 0       // timing experiments only (results are wrong when != 0)
 #endif
@@ -80,7 +83,11 @@ struct RRaw {
 };
 __device__ __forceinline__ RRaw ld_rslot(const RSlot *p, uint64_t policy) {
     RRaw r;
+#if ARE_KR_NOALLOC
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(r.a), "=d"(r.b) : "l"(p), "l"(policy));
+#else
     asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(r.a), "=d"(r.b) : "l"(p), "l"(policy));
+#endif
     return r;
 }
 // mbarrier helpers (shared::cta).  arrive has release and test/try_wait
@@ -257,6 +264,12 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
         const uint32_t e = q[(qh + lane) & (KR_QCAP - 1)];
 #if ARE_KR_EXP == 4  // timing experiment: every gather from a 512 KB window
         return ld_rslot(a.rslots + ((uint32_t)lane < n ? (e & 0x3FFFu) : 0u), pol_keep);
+#endif
+#if ARE_KR_EXP == 7  // timing experiment: every gather from one 128-byte line (L1 hits)
+        return ld_rslot(a.rslots + ((uint32_t)lane < n ? (e & 7u) : 0u), pol_keep);
+#endif
+#if ARE_KR_EXP == 8  // timing experiment: every gather from a 16 KB window (L1-resident)
+        return ld_rslot(a.rslots + ((uint32_t)lane < n ? (e & 1023u) : 0u), pol_keep);
 #endif
 #if ARE_KR_TEX
         // through the texture pipe (the host runs this kernel only with a

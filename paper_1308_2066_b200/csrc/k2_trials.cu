@@ -727,16 +727,20 @@ static int prepare_one() {
     return ARE_OK;
 }
 
-// k2_pair wins on short trials (measured, ms per 1e9 ids, pair vs hotset:
-// E=100 3.57 vs 4.37, E=250 3.04 vs 3.19) and loses on long ones (E=500 2.89
-// vs 2.73, E=1000 2.92 vs 2.52).  ARE_K2_PAIR=0/1 forces a kernel (A/B).
-static constexpr double PAIR_MAX_MEAN_LEN = 320.0;
-static bool use_pair(double mean_len) {
+// k2_pair wins on the shortest trials and loses above ~145 occurrences to
+// the relay kernel (measured, K2 ms per 1e9 ids, C5 J=15, pair vs relay:
+// E=100 3.74 vs 4.08, E=130 3.50 vs 3.64, E=160 3.16 vs 2.97, E=200 3.13 vs
+// 2.53, E=250 3.04 vs 2.53).  Without relay records (no texture) the
+// hot-set kernel runs instead, for which the crossover was 320 (round 1:
+// E=250 3.04 vs 3.19, E=500 2.89 vs 2.73).  ARE_K2_PAIR=0/1 forces a kernel.
+static constexpr double PAIR_MAX_MEAN_LEN = 145.0;
+static constexpr double PAIR_MAX_MEAN_LEN_HOTSET = 320.0;
+static bool use_pair(double mean_len, double limit) {
     static const int force = [] {
         const char *e = getenv("ARE_K2_PAIR");
         return e ? (e[0] == '1' ? 1 : 0) : -1;
     }();
-    return force >= 0 ? force == 1 : mean_len <= PAIR_MAX_MEAN_LEN;
+    return force >= 0 ? force == 1 : mean_len <= limit;
 }
 
 // ARE_DENSE_COOP=0 runs the lane-per-event event-major kernel instead (A/B).
@@ -777,7 +781,7 @@ int k2_prepare(int device) {
 
 template <bool PRE>
 static void launch_hotset(const K2Args &a, int sel, dim3 grid, dim3 block, size_t smem, cudaStream_t st) {
-    if (use_pair(a.mean_len)) {
+    if (use_pair(a.mean_len, PAIR_MAX_MEAN_LEN_HOTSET)) {
         switch (sel) {
             case 0: k2_pair<0, false, PRE><<<grid, block, smem, st>>>(a); break;
             case 1: k2_pair<0, true, PRE><<<grid, block, smem, st>>>(a); break;
@@ -830,7 +834,7 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
     if (g > sms) g = sms;  // persistent: one CTA per SM (the filter fills shared memory)
     const dim3 grid((unsigned)g), block(K2_THREADS);
     const int sel = a.hash_mode * 2 + (check ? 1 : 0);
-    if (a.rslots && a.rtex && !a.precombined && !use_pair(a.mean_len)) {
+    if (a.rslots && a.rtex && !a.precombined && !use_pair(a.mean_len, PAIR_MAX_MEAN_LEN)) {
         // the relay kernel, over its own filter
         K2Args b = a;
         b.filter = a.rfilter;

@@ -55,7 +55,10 @@ struct K2Args {
 // Threads per CTA of the hot-set kernel (one persistent CTA per SM).
 constexpr int K2_THREADS = 1024;
 // Threads per CTA of the relay kernel: 31 producer warps + 1 fold warp.
-constexpr int K2R_THREADS = 1024;
+#ifndef ARE_KR_THREADS
+#define ARE_KR_THREADS 1024
+#endif
+constexpr int K2R_THREADS = ARE_KR_THREADS;
 
 // Fused multi-layer kernel (k2_layers.cu): 16 warps per CTA, up to 16 layers
 // per launch over one ELT pool of up to 64 tables.

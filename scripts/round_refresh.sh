@@ -12,7 +12,7 @@ timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_$TAG.json 2>
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 \
     bench.py --gpus 1 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_torchrun_$TAG.json 2> gpurun_out/bench_torchrun_$TAG.err
 tail -c 300 gpurun_out/bench_torchrun_$TAG.json
-ncu --set full --clock-control none --import-source on -k regex:k2_hotset -s 1 -c 1 -o gpurun_out/k2_$TAG \
+ncu --set full --clock-control none --import-source on -k regex:"k2_(relay|hotset)" -s 1 -c 1 -o gpurun_out/k2_$TAG \
     python scripts/profile_k2.py --launches 2 > gpurun_out/ncu_k2_$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k3_select -s 2 -c 1 -o gpurun_out/k3_$TAG \
     python scripts/profile_k2.py --launches 3 --k3 > gpurun_out/ncu_k3_$TAG.log 2>&1

@@ -37,7 +37,7 @@ def _oracle(yet, stacked, fin, terms):
 
 @pytest.fixture(scope="module")
 def case():
-    # long trials (the relay kernel runs above 320 occurrences per trial) over
+    # long trials (the relay kernel runs above 145 occurrences per trial) over
     # a catalog larger than the shared-memory filter, 6 ELTs with overlap so
     # some events sit in 4+ tables (overflow entries beyond the record)
     spec = GeneratorSpec(seed=77, catalog_size=2_000_000, trial_count=3_000, events_per_trial_range=(400, 1500),
@@ -101,7 +101,7 @@ def test_ragged_trials_across_the_stream(case):
     rng.shuffle(lengths[: len(lengths) // 2])
     offsets = np.zeros(lengths.size + 1, dtype=np.int64)
     np.cumsum(lengths, out=offsets[1:])
-    assert offsets[-1] / lengths.size > 320  # the relay kernel's range
+    assert offsets[-1] / lengths.size > 145  # the relay kernel's range
     src = yet.event_ids
     ids = src[rng.integers(0, src.size, size=int(offsets[-1]))]
     ragged = YearEventTable(yet.catalog_size, ids, None, offsets)
@@ -111,3 +111,24 @@ def test_ragged_trials_across_the_stream(case):
         want = _oracle(ragged, stacked, fin, terms)
         assert got.tobytes() == want.tobytes(), (occ_ret, occ_lim)
         assert lookups == len(elts) * ids.size
+
+
+def test_short_trials_in_the_relay_range(case):
+    """Mean trial lengths just above the k2_pair crossover (145-250
+    occurrences) run the relay kernel: many trials per warp, most final
+    batches partial, some trials with no contributing event at all."""
+    yet, elts, tset, stacked, fin = case
+    from paper_1308_2066_b200.portfolio import YearEventTable
+
+    rng = np.random.default_rng(1308)
+    for lo, hi in [(100, 200), (150, 350)]:
+        lengths = rng.integers(lo, hi, size=12_001)
+        offsets = np.zeros(lengths.size + 1, dtype=np.int64)
+        np.cumsum(lengths, out=offsets[1:])
+        assert 145 < offsets[-1] / lengths.size <= 320
+        ids = yet.event_ids[rng.integers(0, yet.event_ids.size, size=int(offsets[-1]))]
+        short = YearEventTable(yet.catalog_size, ids, None, offsets)
+        for occ_ret, occ_lim in [(500.0, 10_000.0), (9_000.0, 1.0)]:
+            terms = LayerTerms(occ_ret, occ_lim, 1_000.0, 2e6)
+            got, _ = price_layer(short, tset, None, terms)
+            assert got.tobytes() == _oracle(short, stacked, fin, terms).tobytes(), (lo, hi, occ_ret)
