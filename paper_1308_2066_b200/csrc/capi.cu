@@ -384,6 +384,7 @@ static void fill_args(const are_plan_s *p, K2Args &a, double occ_ret, double occ
     a.rhash_mode = p->rhash_mode;
     a.rsmem = p->rsmem;
     a.rtex = p->rb.tex;
+    a.hot_frac = p->tab->row_len > 0 ? (double)p->pb.hot_events / (double)p->tab->row_len : 0.0;
 }
 
 // K2 over trials [first, last) of ids/offsets indexed from id_base/t_base

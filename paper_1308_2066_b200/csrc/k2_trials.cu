@@ -733,8 +733,13 @@ static int prepare_one() {
 // 2.53, E=250 3.04 vs 2.53).  Without relay records (no texture) the
 // hot-set kernel runs instead, for which the crossover was 320 (round 1:
 // E=250 3.04 vs 3.19, E=500 2.89 vs 2.73).  ARE_K2_PAIR=0/1 forces a kernel.
+// Between the two crossovers the relay kernel needs enough hot ids to pay for
+// its hand-off: at E=250 it loses below ~6% hot events (C5, J=1/2/4: pair
+// 1.87/1.88/1.97 vs relay 2.19/2.21/2.21 ms) and wins above (J=8: 2.30 vs
+// 2.22, J=15: 3.05 vs 2.53).
 static constexpr double PAIR_MAX_MEAN_LEN = 145.0;
 static constexpr double PAIR_MAX_MEAN_LEN_HOTSET = 320.0;
+static constexpr double RELAY_MIN_HOT_FRAC_MID = 0.06;
 static bool use_pair(double mean_len, double limit) {
     static const int force = [] {
         const char *e = getenv("ARE_K2_PAIR");
@@ -834,7 +839,8 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
     if (g > sms) g = sms;  // persistent: one CTA per SM (the filter fills shared memory)
     const dim3 grid((unsigned)g), block(K2_THREADS);
     const int sel = a.hash_mode * 2 + (check ? 1 : 0);
-    if (a.rslots && a.rtex && !a.precombined && !use_pair(a.mean_len, PAIR_MAX_MEAN_LEN)) {
+    const double pair_limit = a.hot_frac >= RELAY_MIN_HOT_FRAC_MID ? PAIR_MAX_MEAN_LEN : PAIR_MAX_MEAN_LEN_HOTSET;
+    if (a.rslots && a.rtex && !a.precombined && !use_pair(a.mean_len, pair_limit)) {
         // the relay kernel, over its own filter
         K2Args b = a;
         b.filter = a.rfilter;

@@ -40,6 +40,9 @@ struct K2Args {
     // mean occurrences per trial of the launch (host estimate): short trials
     // run the paired kernel (k2_pair), long ones k2_hotset
     double mean_len;
+    // fraction of catalog events in at least one selected table (plan): the
+    // relay kernel pays off on mid-length trials only when enough ids are hot
+    double hot_frac;
     // relay kernel (k2_relay.cu): its records, fin-applied overflow values
     // and its own filter (its fixed shared memory differs from k2_hotset's)
     const RSlot *rslots = nullptr;
