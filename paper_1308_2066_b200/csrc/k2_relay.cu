@@ -57,6 +57,9 @@ namespace are {
 #ifndef ARE_KR_NOALLOC
 #define ARE_KR_NOALLOC 0   // record gathers (load path) bypass L1 allocation
 #endif
+#ifndef ARE_KR_FOLD_TRYWAIT
+#define ARE_KR_FOLD_TRYWAIT 0  // the fold polls with try_wait (zero suspend hint) instead of test_wait
+#endif
 #ifndef ARE_KR_EXP
 #define ARE_KR_EXP 0       // timing experiments only (results are wrong when != 0)
 #endif
@@ -102,11 +105,19 @@ __device__ __forceinline__ void mbar_arrive(uint32_t a) {
 }
 __device__ __forceinline__ bool mbar_test(uint32_t a, uint32_t parity) {
     uint32_t r;
+#if ARE_KR_FOLD_TRYWAIT
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(r)
+        : "r"(a), "r"(parity)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(r)
         : "r"(a), "r"(parity)
         : "memory");
+#endif
     return r != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {

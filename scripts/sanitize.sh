@@ -13,3 +13,12 @@ D='dense_overlap_plans_event_major_kernel'
 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -x -q -k "$D" 2>&1 | tail -3
 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -x -q -k "$D" 2>&1 | tail -3
 compute-sanitizer --tool synccheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -x -q -k "$D" 2>&1 | tail -3
+# round 2: the relay kernel (k2_relay: TMA filter load, mbarrier ring between producer and fold warps,
+# texture gathers, NaN-tagged records) and the multi-GPU group (per-shard uploads, peer gather).
+# synccheck/racecheck track every mbarrier (148 CTAs x 129): raise their table or they overflow.
+R='ragged_trials_across_the_stream or short_trials_in_the_relay_range or occurrence_terms_sweep'
+compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_relay.py -x -q -k "$R" 2>&1 | tail -3
+compute-sanitizer --tool memcheck --error-exitcode 9 python scripts/relay_small.py 2>&1 | tail -2
+compute-sanitizer --tool synccheck --num-cuda-barriers 40000 --error-exitcode 9 python scripts/relay_small.py 2>&1 | tail -2
+compute-sanitizer --tool racecheck --num-cuda-barriers 40000 --print-limit 4 python scripts/relay_small.py 2>&1 | tail -6
+compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_group.py tests/test_gpu_concurrency.py -x -q 2>&1 | tail -3
