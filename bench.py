@@ -252,6 +252,17 @@ def run_reference_arm(args) -> None:
     sample = args.cpu_sample or calibrate_sample(layer, threads, 90.0 / (args.steps + args.warmup))
     yet = make_yet(0, sample, threads)
     res = cpu_reference(layer, yet, sample, threads, steps=args.steps, warmup=args.warmup)
+    full = None
+    if not args.cpu_sample and not args.no_full_pass:
+        # one pass over the whole C2 workload (1M trials) to pin the sampled
+        # rate: the rate is linear in trials
+        del yet
+        yet_full = make_yet(0, TRIALS_PER_GPU, threads)
+        f = cpu_reference(layer, yet_full, TRIALS_PER_GPU, threads, steps=1)
+        full = {"trials": TRIALS_PER_GPU, "seconds": f["seconds"], "trials_per_s": f["value"],
+                "sampled_over_full": res["value"] / f["value"],
+                "note": "one pass of the full 1M-trial C2 workload after the sampled steps, same kernel and threads"}
+        del yet_full
     line = {
         "metric": METRIC, "value": res["value"], "unit": "trials/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["seconds"] * 1e3,
@@ -261,7 +272,12 @@ def run_reference_arm(args) -> None:
                    "elts": N_ELTS, "catalog": CATALOG, "parallelism": f"{threads} host threads"},
         "cpu_baseline": dict({k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}, host=host_descriptor()),
         "e2e": {"value": res["value"], "unit": "trials/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "same_config": False,
+        "same_config_note": "each step is a bounded sample of the C2 YET (first `sample_trials` trials); "
+                            "`full_pass` times the whole 1M-trial workload once",
     }
+    if full is not None:
+        line["full_pass"] = full
     print(json.dumps(line), flush=True)
 
 
@@ -719,6 +735,7 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-full-pass", action="store_true", help="reference arm: skip the one full 1M-trial pass")
     ap.add_argument("--workload", choices=["c2", "c3", "c4"], default="c2",
                     help="c2: 1M trials per GPU (weak scaling, the headline); c3: the 16-layer portfolio over "
                          "1M trials split across the GPUs; c4: 10M trials split across the GPUs")
