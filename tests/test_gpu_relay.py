@@ -132,3 +132,41 @@ def test_short_trials_in_the_relay_range(case):
             terms = LayerTerms(occ_ret, occ_lim, 1_000.0, 2e6)
             got, _ = price_layer(short, tset, None, terms)
             assert got.tobytes() == _oracle(short, stacked, fin, terms).tobytes(), (lo, hi, occ_ret)
+
+
+def test_nan_inf_and_multi_entry_records():
+    """The 16-byte relay record: one or two entries inline, 3+ entries or a
+    NaN among the first two through the NaN-tagged overflow form.  NaN and
+    +inf losses, zero losses and events in 1-4 tables, long trials (the relay
+    range); NaNs must sit in the same trials, every other value bitwise."""
+    from paper_1308_2066_b200.portfolio import YearEventTable
+
+    rng = np.random.default_rng(4)
+    cat = 5_000
+    elts = []
+    for j in range(4):
+        ids = np.sort(rng.choice(np.arange(1, cat + 1), 2_500, replace=False)).astype(np.uint32)
+        losses = rng.lognormal(0, 1, ids.size) * 300.0
+        losses[rng.random(ids.size) < 0.02] = np.nan
+        losses[rng.random(ids.size) < 0.02] = np.inf
+        losses[rng.random(ids.size) < 0.05] = 0.0
+        elts.append(EventLossTable(cat, ids, losses, FinancialTerms(1.0 + 0.25 * j, 10.0 * j, 4_000.0 if j % 2 else math.inf,
+                                                                     1.0 - 0.1 * j)))
+    tset = TableSet.from_elts(elts, cat)
+    stacked = oracle.dense_tables(elts, cat)
+    fin = [np.array([getattr(e.terms, f) for e in elts], dtype=np.float64)
+           for f in ("exchange_rate", "event_retention", "event_limit", "share")]
+    counts = (stacked[:, 1:] != 0).sum(axis=0)
+    assert counts.max() == 4 and (counts == 2).any() and (counts == 3).any()
+    lengths = rng.integers(300, 600, size=400)
+    offsets = np.zeros(lengths.size + 1, dtype=np.int64)
+    np.cumsum(lengths, out=offsets[1:])
+    yet = YearEventTable(cat, rng.integers(1, cat + 1, int(offsets[-1])).astype(np.uint32), None, offsets)
+    for occ_ret, occ_lim in [(0.0, math.inf), (200.0, 5_000.0)]:
+        terms = LayerTerms(occ_ret, occ_lim, 1_000.0, math.inf)
+        got, _ = price_layer(yet, tset, None, terms)
+        want = _oracle(yet, stacked, fin, terms)
+        assert np.isnan(want).any() and not np.isnan(want).all()
+        assert np.array_equal(np.isnan(got), np.isnan(want))
+        ok = ~np.isnan(want)
+        assert got[ok].tobytes() == want[ok].tobytes(), (occ_ret, occ_lim)
