@@ -147,8 +147,8 @@ def test_nan_inf_and_multi_entry_records():
     for j in range(4):
         ids = np.sort(rng.choice(np.arange(1, cat + 1), 2_500, replace=False)).astype(np.uint32)
         losses = rng.lognormal(0, 1, ids.size) * 300.0
-        losses[rng.random(ids.size) < 0.02] = np.nan
-        losses[rng.random(ids.size) < 0.02] = np.inf
+        losses[rng.choice(ids.size, 3, replace=False)] = np.nan  # few enough that most trials miss them
+        losses[rng.choice(ids.size, 3, replace=False)] = np.inf
         losses[rng.random(ids.size) < 0.05] = 0.0
         elts.append(EventLossTable(cat, ids, losses, FinancialTerms(1.0 + 0.25 * j, 10.0 * j, 4_000.0 if j % 2 else math.inf,
                                                                      1.0 - 0.1 * j)))
