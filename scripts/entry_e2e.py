@@ -26,14 +26,17 @@ engine.run_aggregate_analysis([layer], yet.head(1000))  # library / context warm
 for name, thr in (("host_validate_and_stream", 1 << 62), ("hbm_promoted", engine.PROMOTE_MIN_OCC),
                   ("hbm_promoted_repeat", engine.PROMOTE_MIN_OCC)):
     engine.PROMOTE_MIN_OCC = thr
-    for rep in range(2):
+    runs = []
+    for rep in range(3):
         if name != "hbm_promoted_repeat":
             engine._promoted.clear()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ylts, stats = engine.run_aggregate_analysis_with_stats([layer], yet)
         torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-    res[name] = {"wall_s": wall, "sim_s": stats.sim_seconds, "build_s": stats.build_seconds,
+        runs.append((time.perf_counter() - t0, stats.sim_seconds, stats.build_seconds))
+    best = min(runs)  # host stalls on the shared boxes move single runs by up to ~0.7 s
+    res[name] = {"wall_s": best[0], "sim_s": best[1], "build_s": best[2],
+                 "wall_s_runs": [round(r[0], 4) for r in runs],
                  "pml100": float(np.sort(ylts[0].losses)[-args.trials // 100])}
 print(json.dumps(res))
