@@ -298,7 +298,7 @@ static uint64_t dbits(double x) {
 static int ensure_relay(are_plan_s *p, const DeviceInfo *di, double occ_ret, double occ_lim, cudaStream_t st,
                         const uint32_t **filter) {
     *filter = nullptr;
-    if (p->pool || p->precombined || relay_off()) return ARE_OK;
+    if (p->pool || relay_off()) return ARE_OK;
     std::lock_guard<std::mutex> g(p->relay_mu);
     if (!p->relay_tried) {
         p->relay_tried = true;
@@ -308,7 +308,7 @@ static int ensure_relay(are_plan_s *p, const DeviceInfo *di, double occ_ret, dou
         const int64_t want = ((p->tab->row_len + 127) / 128) * 128;
         int64_t nbits = std::max<int64_t>(std::min(want, max_bits), 128);
         RelayBuffers rb;
-        int rc = k1_build_relay(p->pb, p->d_fin, p->tab->row_len, nbits, rb, di->sms, st);
+        int rc = k1_build_relay(p->pb, p->d_fin, p->tab->row_len, nbits, rb, di->sms, st, p->precombined);
         // other streams may use the plan next: the records must be complete
         if (rc == ARE_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "relay records");
         if (rc) {

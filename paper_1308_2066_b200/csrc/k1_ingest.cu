@@ -161,7 +161,8 @@ int k1_precombine_plan(PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int s
 // taken here, so K2 adds f_{j2}, f_{j3}, ... in selection order exactly as
 // the reference's comb loop does (_kernel.pyx:69-76).
 __global__ void k1_relay_slots(const Slot *__restrict__ slots, const Entry *__restrict__ ovf,
-                               const Fin *__restrict__ fin, int64_t row_len, RSlot *__restrict__ rs) {
+                               const Fin *__restrict__ fin, int64_t row_len, RSlot *__restrict__ rs,
+                               bool precombined) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < row_len;
          e += (int64_t)gridDim.x * blockDim.x) {
         const Slot s = slots[e];
@@ -169,7 +170,16 @@ __global__ void k1_relay_slots(const Slot *__restrict__ slots, const Entry *__re
         RSlot r;
         r.a = 0.0;
         r.b = 0.0;
-        if (cnt) {
+        if (cnt && precombined) {
+            // the record already holds comb = 0.0 + sum_j fin_j(x_j) (k1_precombine;
+            // never -0.0): comb + (+0.0) is comb, a NaN comb takes the tagged form
+            if (!(s.x != s.x)) {
+                r.a = s.x;
+            } else {
+                r.a = __longlong_as_double((long long)(RSLOT_COMPLEX | (1ull << 32)));
+                r.b = s.x;
+            }
+        } else if (cnt) {
             const double x0 = __dadd_rn(0.0, fin_term(fin[s.meta & 0xFFFFu], s.x));
             const double f1 = cnt >= 2 ? fin_term(fin[ovf[s.ovf].j], ovf[s.ovf].x) : 0.0;
             if (cnt <= 2 && !(x0 != x0) && !(f1 != f1)) {
@@ -202,7 +212,7 @@ __global__ void k1_relay_ovf(const Entry *__restrict__ ovf, const Fin *__restric
 }
 
 int k1_build_relay(const PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int64_t filter_bits, RelayBuffers &rb,
-                   int sms, cudaStream_t st) {
+                   int sms, cudaStream_t st, bool precombined) {
     const int64_t n_ovf = std::max<int64_t>(pb.overflow_entries, 1);
     if (cudaMalloc(&rb.rslots, row_len * sizeof(RSlot)) != cudaSuccess ||
         cudaMalloc(&rb.rovf, n_ovf * sizeof(double)) != cudaSuccess) {
@@ -210,9 +220,10 @@ int k1_build_relay(const PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int
         rb.release();
         return fail(ARE_ENOMEM, "device allocation failed while building the relay records");
     }
-    k1_relay_slots<<<grid_for(row_len, 256, sms), 256, 0, st>>>(pb.slots, pb.ovf, d_fin, row_len, rb.rslots);
+    k1_relay_slots<<<grid_for(row_len, 256, sms), 256, 0, st>>>(pb.slots, pb.ovf, d_fin, row_len, rb.rslots,
+                                                                precombined);
     ARE_LAUNCHED();
-    if (pb.overflow_entries) {
+    if (pb.overflow_entries && !precombined) {
         k1_relay_ovf<<<grid_for(pb.overflow_entries, 256, sms), 256, 0, st>>>(pb.ovf, d_fin, pb.overflow_entries,
                                                                                rb.rovf);
         ARE_LAUNCHED();

@@ -30,7 +30,7 @@ struct RelayBuffers {
 };
 
 int k1_build_relay(const PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int64_t filter_bits, RelayBuffers &rb,
-                   int sms, cudaStream_t st);
+                   int sms, cudaStream_t st, bool precombined = false);
 
 // The relay filter for one pair of occurrence terms: bit b set iff some
 // event e with hash(e) == b has an occurrence value that is not +-0 under

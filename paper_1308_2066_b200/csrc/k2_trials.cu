@@ -840,7 +840,7 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
     const dim3 grid((unsigned)g), block(K2_THREADS);
     const int sel = a.hash_mode * 2 + (check ? 1 : 0);
     const double pair_limit = a.hot_frac >= RELAY_MIN_HOT_FRAC_MID ? PAIR_MAX_MEAN_LEN : PAIR_MAX_MEAN_LEN_HOTSET;
-    if (a.rslots && a.rtex && !a.precombined && !use_pair(a.mean_len, pair_limit)) {
+    if (a.rslots && a.rtex && !use_pair(a.mean_len, pair_limit)) {
         // the relay kernel, over its own filter
         K2Args b = a;
         b.filter = a.rfilter;
