@@ -737,9 +737,15 @@ static int prepare_one() {
 // its hand-off: at E=250 it loses below ~6% hot events (C5, J=1/2/4: pair
 // 1.87/1.88/1.97 vs relay 2.19/2.21/2.21 ms) and wins above (J=8: 2.30 vs
 // 2.22, J=15: 3.05 vs 2.53).
+// Below 145 the relay kernel still wins when many ids are hot, down to ~64
+// occurrences (E=100: J=15, 14% hot: pair 3.74 vs relay 4.09 ms; J=32, 27%:
+// 5.42 vs 4.30; J=64: 8.29 vs 5.94.  E=30: J=32 8.14 vs 12.66, J=64 11.61 vs
+// 13.12 -- there the per-trial flush through the fold dominates).
 static constexpr double PAIR_MAX_MEAN_LEN = 145.0;
 static constexpr double PAIR_MAX_MEAN_LEN_HOTSET = 320.0;
 static constexpr double RELAY_MIN_HOT_FRAC_MID = 0.06;
+static constexpr double RELAY_MIN_HOT_FRAC_SHORT = 0.20;
+static constexpr double RELAY_MIN_MEAN_LEN_SHORT = 64.0;
 static bool use_pair(double mean_len, double limit) {
     static const int force = [] {
         const char *e = getenv("ARE_K2_PAIR");
@@ -839,7 +845,8 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
     if (g > sms) g = sms;  // persistent: one CTA per SM (the filter fills shared memory)
     const dim3 grid((unsigned)g), block(K2_THREADS);
     const int sel = a.hash_mode * 2 + (check ? 1 : 0);
-    const double pair_limit = a.hot_frac >= RELAY_MIN_HOT_FRAC_MID ? PAIR_MAX_MEAN_LEN : PAIR_MAX_MEAN_LEN_HOTSET;
+    const double pair_limit = a.hot_frac >= RELAY_MIN_HOT_FRAC_SHORT ? RELAY_MIN_MEAN_LEN_SHORT
+                              : a.hot_frac >= RELAY_MIN_HOT_FRAC_MID ? PAIR_MAX_MEAN_LEN : PAIR_MAX_MEAN_LEN_HOTSET;
     if (a.rslots && a.rtex && !use_pair(a.mean_len, pair_limit)) {
         // the relay kernel, over its own filter
         K2Args b = a;
