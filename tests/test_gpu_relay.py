@@ -162,11 +162,15 @@ def test_nan_inf_and_multi_entry_records():
     offsets = np.zeros(lengths.size + 1, dtype=np.int64)
     np.cumsum(lengths, out=offsets[1:])
     yet = YearEventTable(cat, rng.integers(1, cat + 1, int(offsets[-1])).astype(np.uint32), None, offsets)
+    from paper_1308_2066_b200.engine import EngineConfig
+
     for occ_ret, occ_lim in [(0.0, math.inf), (200.0, 5_000.0)]:
         terms = LayerTerms(occ_ret, occ_lim, 1_000.0, math.inf)
-        got, _ = price_layer(yet, tset, None, terms)
         want = _oracle(yet, stacked, fin, terms)
         assert np.isnan(want).any() and not np.isnan(want).all()
-        assert np.array_equal(np.isnan(got), np.isnan(want))
-        ok = ~np.isnan(want)
-        assert got[ok].tobytes() == want[ok].tobytes(), (occ_ret, occ_lim)
+        # exact records, and pre-combined ones ({comb, +0.0}; a NaN comb tagged)
+        for cfg in (EngineConfig(), EngineConfig(precombine=True)):
+            got, _ = price_layer(yet, tset, None, terms, cfg)
+            assert np.array_equal(np.isnan(got), np.isnan(want)), cfg
+            ok = ~np.isnan(want)
+            assert got[ok].tobytes() == want[ok].tobytes(), (occ_ret, occ_lim, cfg)
