@@ -642,6 +642,28 @@ def run_ours(args) -> None:
         pcie.append(pinned_ids.numel() * 4 / (ev[0].elapsed_time(ev[1]) / 1e3) / 1e9)
     del d_probe
     pcie_gbs = max(pcie)
+    if workload == "c2" and world == 1:
+        # the validated entry point on the same host YET:
+        # run_aggregate_analysis promotes it to HBM (upload + K0 validation of
+        # ids and trial lengths), then K1 + K2 + D2H; again on the same YET
+        # object its validated device copy is reused
+        from paper_1308_2066_b200.engine import run_aggregate_analysis_with_stats
+        from paper_1308_2066_b200.portfolio import YearEventTable
+
+        y = YearEventTable(CATALOG, hyet.event_ids, None, hyet.offsets)
+        ep = []
+        for _ in range(3):
+            torch.cuda.synchronize(dev)
+            t_ep = time.perf_counter()
+            _, st_ep = run_aggregate_analysis_with_stats([layer], y)
+            ep.append((time.perf_counter() - t_ep, st_ep.sim_seconds))
+        side["entry_point"] = {
+            "cold_s": ep[0][0], "repeat_s": min(e[0] for e in ep[1:]), "sim_s": min(e[1] for e in ep),
+            "trials": e2e_trials,
+            "note": "run_aggregate_analysis([layer], host YET of this rank): the first call uploads the 4 GB of "
+                    "ids and validates them on the device (K0), later calls on the same YET object reuse "
+                    "the validated device copy; the reference validates on the host (~9 s at C2)"}
+        del y
     n_layers_out = 16 if workload == "c3" else 1
     h2d = int(hyet.event_ids.nbytes + hyet.offsets.nbytes + e2e_trials * 8 * n_layers_out)
     d2h = int(e2e_trials * 8 * n_layers_out + 2 * 8 * len(RPS))

@@ -174,3 +174,18 @@ def test_nan_inf_and_multi_entry_records():
             assert np.array_equal(np.isnan(got), np.isnan(want)), cfg
             ok = ~np.isnan(want)
             assert got[ok].tobytes() == want[ok].tobytes(), (occ_ret, occ_lim, cfg)
+
+
+def test_out_of_range_id_in_a_long_trial_raises(case):
+    """The relay kernel's per-id range check (unvalidated host YETs): an id
+    beyond the catalog inside a long trial raises EventOutOfRangeError, as
+    the reference's analyse_trial / validation would."""
+    yet, elts, tset, stacked, fin = case
+    from paper_1308_2066_b200.errors import EventOutOfRangeError
+    from paper_1308_2066_b200.portfolio import YearEventTable
+
+    ids = np.array(yet.event_ids[: 600 * 50], dtype=np.uint32)
+    ids[12_345] = yet.catalog_size + 7
+    bad = YearEventTable(yet.catalog_size, ids, None, np.arange(51, dtype=np.int64) * 600)
+    with pytest.raises(EventOutOfRangeError):
+        price_layer(bad, tset, None, LayerTerms(500.0, 10_000.0, 1_000.0, 2e6))
