@@ -472,6 +472,8 @@ struct SortCache {
     int64_t rank_cap = 0;
     int64_t *d_ranks = nullptr;
     double *d_out = nullptr;
+    int64_t *h_ranks = nullptr;  // pinned staging: the copies stay asynchronous
+    double *h_out = nullptr;
 };
 static SortCache g_sort[64];
 
@@ -504,24 +506,34 @@ int k3_pml_sorted(const double *d_x, int64_t n, const double *rps, int64_t n_rp,
     if (n_rp > c.rank_cap) {
         cudaFree(c.d_ranks);
         cudaFree(c.d_out);
+        cudaFreeHost(c.h_ranks);
+        cudaFreeHost(c.h_out);
         c.d_ranks = nullptr;
         c.d_out = nullptr;
+        c.h_ranks = nullptr;
+        c.h_out = nullptr;
         c.rank_cap = 0;
         ARE_CUDA(cudaMalloc(&c.d_ranks, sizeof(int64_t) * (size_t)n_rp));
         ARE_CUDA(cudaMalloc(&c.d_out, sizeof(double) * (size_t)n_rp));
+        ARE_CUDA(cudaHostAlloc(&c.h_ranks, sizeof(int64_t) * (size_t)n_rp, cudaHostAllocDefault));
+        ARE_CUDA(cudaHostAlloc(&c.h_out, sizeof(double) * (size_t)n_rp, cudaHostAllocDefault));
         c.rank_cap = n_rp;
     }
+    // every copy from/to pinned staging, the ranks first: nothing waits on the
+    // host between the launches (a pageable copy would sync the stream first)
+    std::memcpy(c.h_ranks, ranks.data(), sizeof(int64_t) * (size_t)n_rp);
+    ARE_CUDA(cudaMemcpyAsync(c.d_ranks, c.h_ranks, sizeof(int64_t) * (size_t)n_rp, cudaMemcpyHostToDevice, st));
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
     k3_keys<<<blocks, 256, 0, st>>>(d_x, n, c.d_keys);
     ARE_LAUNCHED();
     size_t tmp = c.tmp_bytes;
     ARE_CUDA(cub::DeviceRadixSort::SortKeys(c.d_tmp, tmp, c.d_keys, c.d_keys + c.cap, n, 0, 64, st));
-    ARE_CUDA(cudaMemcpyAsync(c.d_ranks, ranks.data(), sizeof(int64_t) * (size_t)n_rp, cudaMemcpyHostToDevice, st));
     k3_gather_ranks<<<(int)std::min<int64_t>((n_rp + 255) / 256, 1024), 256, 0, st>>>(c.d_keys + c.cap, c.d_ranks,
                                                                                        (int)n_rp, c.d_out);
     ARE_LAUNCHED();
-    ARE_CUDA(cudaMemcpyAsync(pml_out, c.d_out, sizeof(double) * (size_t)n_rp, cudaMemcpyDeviceToHost, st));
+    ARE_CUDA(cudaMemcpyAsync(c.h_out, c.d_out, sizeof(double) * (size_t)n_rp, cudaMemcpyDeviceToHost, st));
     ARE_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(pml_out, c.h_out, sizeof(double) * (size_t)n_rp);
     return ARE_OK;
 }
 

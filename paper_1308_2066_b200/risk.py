@@ -32,6 +32,14 @@ def _order_stat_k(n: int, return_period: float) -> int:
     return n - math.floor(n / rp)
 
 
+def _check_rps(n: int, rps: np.ndarray) -> None:
+    """_order_stat_k's checks for every return period at once; the first
+    offending one raises the reference's message."""
+    bad = ~(rps > 1.0) | (rps > n)
+    if bad.any():
+        _order_stat_k(n, float(rps[int(np.argmax(bad))]))
+
+
 def _is_cuda_tensor(x) -> bool:
     return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda"))
 
@@ -55,8 +63,7 @@ def order_stats(ylt, return_periods: Sequence[float], stream=None) -> tuple[np.n
     if n == 0:
         raise ValueError("empty year loss table")
     rps = np.ascontiguousarray([float(r) for r in return_periods], dtype=np.float64)
-    for r in rps:
-        _order_stat_k(n, r)
+    _check_rps(n, rps)
     pml_out = np.empty(rps.size)
     tvar_out = np.empty(rps.size)
     if rps.size == 0:
@@ -88,9 +95,8 @@ def pml_many(ylt, return_periods: Sequence[float], stream=None) -> np.ndarray:
     n = int(src.shape[0])
     if n == 0:
         raise ValueError("empty year loss table")
-    rps = np.ascontiguousarray([float(r) for r in return_periods], dtype=np.float64)
-    for r in rps:
-        _order_stat_k(n, r)
+    rps = np.ascontiguousarray(return_periods, dtype=np.float64).reshape(-1)
+    _check_rps(n, rps)
     if rps.size < SORT_MIN_RPS:
         return order_stats(src, rps, stream)[0]
     import torch
@@ -114,8 +120,7 @@ def order_stats_summary(d_ylt, return_periods: Sequence[float], stream=None):
     if n == 0:
         raise ValueError("empty year loss table")
     rps = np.ascontiguousarray([float(r) for r in return_periods], dtype=np.float64)
-    for r in rps:
-        _order_stat_k(n, r)
+    _check_rps(n, rps)
     pml_out = np.empty(max(rps.size, 1))
     tvar_out = np.empty(max(rps.size, 1))
     mm = np.empty(2)
@@ -153,6 +158,22 @@ class EPCurve:
         if any(not 0.0 <= p <= 1.0 for _, p in pts):
             raise ValueError("probability outside [0, 1]")
 
+    @classmethod
+    def _from_arrays(cls, loss: np.ndarray, prob: np.ndarray) -> "EPCurve":
+        """The same invariants checked on arrays (first failing pair first),
+        for curves built from one device pass: no per-point Python loop."""
+        p_bad = ~(prob[1:] < prob[:-1])
+        l_bad = loss[1:] < loss[:-1]
+        if p_bad.any() or l_bad.any():
+            ip = int(np.argmax(p_bad)) if p_bad.any() else prob.size
+            il = int(np.argmax(l_bad)) if l_bad.any() else prob.size
+            raise ValueError("probabilities must be strictly decreasing" if ip <= il else "losses must be non-decreasing")
+        if not np.all((prob >= 0.0) & (prob <= 1.0)):
+            raise ValueError("probability outside [0, 1]")
+        self = object.__new__(cls)
+        object.__setattr__(self, "points", tuple(zip(loss.tolist(), prob.tolist())))
+        return self
+
     @property
     def losses(self) -> tuple:
         return tuple(l for l, _ in self.points)
@@ -176,8 +197,9 @@ def ep_curve(ylt, return_periods: Iterable[float]) -> EPCurve:
     rps = sorted({float(r) for r in return_periods})
     if not rps:
         raise ValueError("no return periods given")
-    p = pml_many(src, rps)
-    return EPCurve(tuple((float(v), 1.0 / rp) for v, rp in zip(p, rps)))
+    rp_arr = np.asarray(rps, dtype=np.float64)
+    p = pml_many(src, rp_arr)
+    return EPCurve._from_arrays(np.asarray(p, dtype=np.float64), 1.0 / rp_arr)
 
 
 def portfolio_rollup(ylts: Sequence[YearLossTable]) -> YearLossTable:
