@@ -698,7 +698,7 @@ int are_plan_info(are_plan_t p, are_plan_info_t *info) {
     info->zero_skip_exact = (p->zero_skip && !p->slot0_hot) ? 1 : 0;
     info->smem_bytes = (int32_t)p->smem;
     std::lock_guard<std::mutex> g(p->relay_mu);
-    info->relay = p->rb.rslots && p->rb.tex ? 1 : 0;
+    info->relay = p->rb.rslots && (p->rb.tex || !k2_relay_needs_texture()) ? 1 : 0;
     info->relay_filter_bits = p->rb.rslots ? p->rnbits : 0;
     info->relay_smem_bytes = p->rb.rslots ? (int32_t)p->rsmem : 0;
     return ARE_OK;

@@ -54,7 +54,7 @@ struct __align__(16) Entry {
 };
 
 // Relay-kernel record (k2_relay.cu), one per event id, 16 bytes (one
-// texture texel): the event's selected entries with the financial terms
+// 128-bit load): the event's selected entries with the financial terms
 // already applied by K1, f_j(x_j) = share_j * clamp(rate_j * x_j - ret_j, 0,
 // lim_j) in selection order j1 < j2 < ...
 //   simple event (at most 2 entries, none NaN):

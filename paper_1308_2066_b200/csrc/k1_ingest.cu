@@ -17,6 +17,7 @@
 //
 // All passes are deterministic (no order-dependent atomics on data).
 #include "k1_ingest.cuh"
+#include "k2_trials.cuh"
 
 namespace are {
 
@@ -229,7 +230,7 @@ int k1_build_relay(const PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int
         ARE_LAUNCHED();
     }
     rb.filter_words = (filter_bits + 31) / 32;  // the per-terms filters (k1_relay_filter)
-    if (row_len <= (int64_t)1 << 27) {  // linear textures hold up to 2^27 texels
+    if (k2_relay_needs_texture() && row_len <= (int64_t)1 << 27) {  // linear textures hold up to 2^27 texels
         cudaResourceDesc rd{};
         rd.resType = cudaResourceTypeLinear;
         rd.res.linear.devPtr = rb.rslots;

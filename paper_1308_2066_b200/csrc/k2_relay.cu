@@ -18,7 +18,7 @@
 //     ...: they stream the trial's ids (32-id coalesced rows, two 128-id
 //     chunks in flight), test each id against the shared-memory filter,
 //     append the hot ones in trial order to a per-warp queue, and per 32
-//     queued events gather one 16-byte record per lane (one texture texel:
+//     queued events gather one 16-byte record per lane (one LDG.128:
 //     the event's first partial sum and its second entry, or a tagged
 //     pointer to its entries for the rare events with 3+; common.cuh RSlot)
 //     and compute the event's occurrence value.  The 32 values go to the
@@ -49,13 +49,13 @@ namespace are {
 #define ARE_KR_ROWDRAIN 0  // drain the queue after every row (64-entry queue) instead of every two
 #endif
 #ifndef ARE_KR_TEX
-#define ARE_KR_TEX 1       // gather the records through the texture pipe (tex1Dfetch): off the LSU pipe the kernel is bound by
+#define ARE_KR_TEX 0       // 1: gather the records through the texture pipe (tex1Dfetch) instead of LDG
 #endif
 #ifndef ARE_KR_TMAF
 #define ARE_KR_TMAF 1      // the filter enters shared memory by TMA bulk copies (one thread, no register staging)
 #endif
 #ifndef ARE_KR_NOALLOC
-#define ARE_KR_NOALLOC 0   // record gathers (load path) bypass L1 allocation
+#define ARE_KR_NOALLOC 1   // record gathers (load path) bypass L1 allocation
 #endif
 #ifndef ARE_KR_FOLD_TRYWAIT
 #define ARE_KR_FOLD_TRYWAIT 0  // the fold polls with try_wait (zero suspend hint) instead of test_wait
@@ -430,6 +430,8 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
 #endif
     if (CHECK && __any_sync(0xffffffffu, emax > last_id) && lane == 0) atomicOr(a.err, 1u);
 }
+
+bool k2_relay_needs_texture() { return ARE_KR_TEX != 0; }
 
 int k2_relay_prepare() {
     ARE_CUDA(cudaFuncSetAttribute(k2_relay<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));

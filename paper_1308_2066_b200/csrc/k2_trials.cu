@@ -847,7 +847,7 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
     const int sel = a.hash_mode * 2 + (check ? 1 : 0);
     const double pair_limit = a.hot_frac >= RELAY_MIN_HOT_FRAC_SHORT ? RELAY_MIN_MEAN_LEN_SHORT
                               : a.hot_frac >= RELAY_MIN_HOT_FRAC_MID ? PAIR_MAX_MEAN_LEN : PAIR_MAX_MEAN_LEN_HOTSET;
-    if (a.rslots && a.rtex && !use_pair(a.mean_len, pair_limit)) {
+    if (a.rslots && (a.rtex || !k2_relay_needs_texture()) && !use_pair(a.mean_len, pair_limit)) {
         // the relay kernel, over its own filter
         K2Args b = a;
         b.filter = a.rfilter;

@@ -99,6 +99,7 @@ __device__ __forceinline__ uint32_t cold_pad(const uint32_t *s_filter, int64_t f
 // Largest dynamic shared-memory carve-out requested by K2 (sm_100: 227 KB).
 inline int k2_max_dynamic_smem() { return 227 * 1024; }
 size_t k2_hotset_fixed_smem(int n_sel);
+bool k2_relay_needs_texture();  // the relay build gathers through a texture object
 int k2_prepare(int device);
 int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStream_t st);
 size_t k2_relay_fixed_smem();
