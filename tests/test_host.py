@@ -190,6 +190,46 @@ def test_ep_curve_invariants():
     assert list(c) == [(500.0, 0.5), (900.0, 0.1)] and c.losses == (500.0, 900.0)
 
 
+def test_ep_curve_array_constructor_matches_the_pairwise_checks(rng):
+    """EPCurve._from_arrays (the device EP path) raises exactly what the
+    reference's pairwise __post_init__ loop raises, first failure first."""
+    cases = [([1.0, 2.0, 3.0], [0.5, 0.2, 0.1]), ([1.0, 0.5], [0.5, 0.4]), ([1.0, 2.0], [0.5, 0.5]),
+             ([2.0, 1.0, 3.0], [0.5, 0.6, 0.1]), ([1.0, 2.0], [1.5, 0.4]), ([1.0, float("nan")], [0.5, 0.1]),
+             ([1.0, 2.0], [0.5, float("nan")]), ([5.0], [0.25])]
+    for _ in range(200):
+        n = int(rng.integers(1, 6))
+        cases.append((list(np.round(rng.normal(0, 1, n), 1)), list(np.round(rng.uniform(-0.2, 1.2, n), 1))))
+    for loss, prob in cases:
+        def run(f):
+            try:
+                return f().points
+            except ValueError as e:
+                return str(e)
+        want = run(lambda: EPCurve(tuple(zip(loss, prob))))
+        got = run(lambda: EPCurve._from_arrays(np.asarray(loss, float), np.asarray(prob, float)))
+        assert got == want or (isinstance(got, tuple) and str(got) == str(want)), (loss, prob, got, want)
+
+
+def test_return_period_checks_match_the_scalar_rule():
+    from paper_1308_2066_b200.risk import _check_rps, _order_stat_k
+
+    for rps in ([2.0, 10.0], [1.0], [0.5, 3.0], [5.0, 2e6], [float("nan")], [3.0, 1e6, 1.0]):
+        arr = np.asarray(rps, dtype=np.float64)
+        want = None
+        for r in rps:
+            try:
+                _order_stat_k(1_000_000, r)
+            except ValueError as e:
+                want = str(e)
+                break
+        try:
+            _check_rps(1_000_000, arr)
+            got = None
+        except ValueError as e:
+            got = str(e)
+        assert got == want, rps
+
+
 # --------------------------------------------------------- the C-ABI .so --
 
 def _declared_symbols() -> list[str]:
