@@ -86,7 +86,11 @@ struct RRaw {
 };
 __device__ __forceinline__ RRaw ld_rslot(const RSlot *p, uint64_t policy) {
     RRaw r;
-#if ARE_KR_NOALLOC
+#if ARE_KR_NOALLOC == 2  // A/B: L2-only load (.cg)
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(r.a), "=d"(r.b) : "l"(p), "l"(policy));
+#elif ARE_KR_NOALLOC == 3  // A/B: allocate, evict first
+    asm volatile("ld.global.nc.L1::evict_first.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(r.a), "=d"(r.b) : "l"(p), "l"(policy));
+#elif ARE_KR_NOALLOC
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(r.a), "=d"(r.b) : "l"(p), "l"(policy));
 #else
     asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(r.a), "=d"(r.b) : "l"(p), "l"(policy));
