@@ -97,14 +97,19 @@ def _peaks() -> tuple[float, str]:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def _traffic(kernel: str) -> float | None:
-    """DRAM bytes per K2 launch from the committed ncu capture of `kernel`, if any."""
+def _traffic(kernel: str, key: str = "dram_bytes_per_launch") -> float | None:
+    """Per-launch figure of K2 from the committed ncu capture of `kernel`, if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "k2_traffic.json")) as f:
             d = json.load(f)
-        return float(d["dram_bytes_per_launch"]) if d.get("kernel", "k2_hotset") == kernel else None
+        return float(d[key]) if d.get("kernel", "k2_hotset") == kernel and d.get(key) is not None else None
     except Exception:
         return None
+
+
+# Scattered-sector throughput of one B200 measured alone (DESIGN.md §4, K2-R):
+# random 16-byte loads from an L2-resident table, scripts/micro/gather_rate.cu
+SECTOR_PEAK_G_PER_S = 186.0
 
 
 class ClockSampler:
@@ -351,6 +356,22 @@ def compulsory_bytes_per_trial(events: int = EVENTS) -> int:
     return 4 * events + 8 + 8
 
 
+def _sector_roofline(kernel: str, kernel_ms: float, trials: int) -> dict | None:
+    """K2's binding bound: every id row and every record gather is an L2
+    sector read through the SM's memory path (ids + records, ncu
+    lts__t_sectors_srcunit_tex_op_read of the committed capture, 1M trials)."""
+    sectors = _traffic(kernel, "l2_read_sectors_per_launch")
+    if sectors is None:
+        return None
+    sectors *= trials / TRIALS_PER_GPU
+    achieved = sectors / (kernel_ms / 1e3) / 1e9
+    return {"sectors_per_launch": sectors, "achieved": achieved, "peak": SECTOR_PEAK_G_PER_S, "unit": "G sectors/s",
+            "frac": achieved / SECTOR_PEAK_G_PER_S,
+            "peak_source": "measured: scripts/micro/gather_rate.cu (random 16-byte L2 reads, nothing else running)",
+            "note": "ids (125M sectors per 1M trials) and relay-record gathers share the SM's L2 read path; "
+                    "this, not HBM bandwidth, bounds K2 (DESIGN.md section 4)"}
+
+
 def roofline(trials: int, kernel_ms: float, kernel: str) -> dict:
     """K2's roofline on the bytes that cross HBM (the verdict's rule: the
     lookups are served from L2 / shared memory by design, so the SURVEY 8(d)
@@ -368,6 +389,7 @@ def roofline(trials: int, kernel_ms: float, kernel: str) -> dict:
         "peak_source": peak_src,
         "traffic_note": "ncu dram__bytes_read+write per 1M-trial launch (profiles/k2_traffic.json); "
                         "traffic_ratio = traffic / bytes_per_launch at 1M trials",
+        "sector_throughput": _sector_roofline(kernel, kernel_ms, trials),
         "lookup_equivalent": {
             "bytes_per_launch": lk, "formula": "trials x (12 + 4*E*(1+J)), SURVEY.md 8(d)",
             "gbs": lk / (kernel_ms / 1e3) / 1e9, "ratio_to_peak": lk / (kernel_ms / 1e3) / 1e9 / peak,

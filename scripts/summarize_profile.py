@@ -117,7 +117,9 @@ def main() -> None:
         with open(args.traffic_json, "w") as f:
             name = m["Kernel Name"][0] if "Kernel Name" in m else ""
             kernel = next((k for k in ("k2_relay", "k2_hotset", "k2_pair", "k2_dense") if k in name), name)
+            l2_sectors = val("lts__t_sectors_srcunit_tex_op_read.sum") if "lts__t_sectors_srcunit_tex_op_read.sum" in m else None
             json.dump({"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                       "l2_read_sectors_per_launch": l2_sectors,
                        "duration_s": dur, "report": args.rep, "kernel": kernel}, f, indent=1)
     print("\n".join(lines[:14]))
 
