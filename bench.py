@@ -473,7 +473,7 @@ def run_ours(args) -> None:
     from paper_1308_2066_b200.distributed import allgather_portfolio, allgather_ylt, max_over_ranks, partition
     from paper_1308_2066_b200.engine import layer_pool, price_layer, simulate_layers_device
     from paper_1308_2066_b200.resident import DeviceYearEventTable
-    from paper_1308_2066_b200.risk import order_stats, rollup_device
+    from paper_1308_2066_b200.risk import order_stats, order_stats_async, rollup_device
 
     workload = args.workload
     world, rank, backend, local, dev = _setup_dist()
@@ -537,8 +537,49 @@ def run_ours(args) -> None:
             ev[3].record(stream)
         return res
 
-    for _ in range(args.warmup):
-        step()
+    # Pipelined steps (c2, c4): step i's K2 runs on `stream` over all but k SMs
+    # (ARE_SPARE_SMS(k)) while step i-1's exchange and K3 run on `side` over
+    # the k spare SMs (2 CTAs each, no host wait), each step writing its own
+    # YLT buffer (two, reused once the K3 that read them is done) and result
+    # row.  k grows with the table K3 reads (this rank's YLT after the
+    # exchange) relative to the trials K2 processes, so the overlapped K3
+    # stays shorter than K2: 1 at N=1, N on N GPUs.  It pays while the YLT K3
+    # streams stays small next to L2 (C2 on one GPU: 8 MB, +4%); with C4's
+    # 80 MB YLT the overlapped K3 evicts K2's records from L2 and K2 slows by
+    # more than K3 costs, so the headline steps stay sequential (--pipeline
+    # times pipelined steps instead; the C2 line reports them beside).
+    pipelined = workload != "c3" and args.pipeline
+    can_pipeline = workload != "c3"
+    spare = max(1, -(-(total_trials if world > 1 else n_local) // max(n_local, 1)))
+    if can_pipeline:
+        side = torch.cuda.Stream(dev)
+        bufs = [d_local, torch.empty_like(d_local)]
+        d_res = torch.zeros((args.warmup + args.steps, 16), dtype=torch.float64, device=dev)
+        freed = [None, None]
+
+        def pstep(i, ev):
+            b = i & 1
+            if freed[b] is not None:
+                stream.wait_event(freed[b])  # the K3 that last read this buffer is done
+            ev[0].record(stream)
+            dyet.simulate_device(plan, layer.terms, out=bufs[b], stream=stream, check=False,
+                                 flags=_native.spare_sms(spare))
+            ev[1].record(stream)
+            side.wait_event(ev[1])
+            with torch.cuda.stream(side):
+                full = allgather_ylt(bufs[b], parts) if world > 1 else bufs[b]
+                ev[2].record(side)
+                order_stats_async(full, RPS, d_res[i], side, max_ctas=2 * spare)
+                ev[3].record(side)
+            freed[b] = ev[3]
+
+    if pipelined:
+        wev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.warmup)]
+        for i in range(args.warmup):
+            pstep(i, wev[i])
+    else:
+        for _ in range(args.warmup):
+            step()
     _native.check(_native.load().are_check_errors(plan.value, None))
     torch.cuda.synchronize(dev)
     if workload != "c3":
@@ -553,22 +594,73 @@ def run_ours(args) -> None:
         torch.cuda.synchronize(dev)
         start.record(stream)
         for i in range(args.steps):
-            pml_v, tvar_v = step(evs[i])
+            if pipelined:
+                pstep(args.warmup + i, evs[i])
+            else:
+                pml_v, tvar_v = step(evs[i])
+        if pipelined:
+            stream.wait_event(evs[-1][3])  # the last step's K3
         stop.record(stream)
         torch.cuda.synchronize(dev)
     launches = _native.launch_count() - launches0
+    pipelined_side = None
+    if not pipelined and can_pipeline and world == 1 and workload == "c2":
+        # the same steps pipelined, reported beside the sequential headline
+        pev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.warmup + 20)]
+        for i in range(args.warmup):
+            pstep(i, pev[i])
+        torch.cuda.synchronize(dev)
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for i in range(args.warmup, args.warmup + 20):
+            pstep(i % d_res.shape[0], pev[i])
+        stream.wait_event(pev[-1][3])
+        p1.record(stream)
+        torch.cuda.synchronize(dev)
+        pms = p0.elapsed_time(p1) / 20
+        last = d_res[(args.warmup + 19) % d_res.shape[0]].cpu().numpy()
+        assert list(last[: len(RPS)]) == list(pml_v), "pipelined and sequential K3 disagree"
+        pipelined_side = {
+            "value": total_trials / (pms / 1e3), "ms_per_step": pms, "spare_sms": spare,
+            "k2_ms": float(np.mean([e[0].elapsed_time(e[1]) for e in pev[args.warmup:]])),
+            "k3_overlapped_ms": float(np.mean([e[2].elapsed_time(e[3]) for e in pev[args.warmup:]])),
+            "note": "the same steps pipelined (bench.py --pipeline): step i's K3 on the SM K2 leaves free "
+                    "(are_order_stats_async, 2 CTAs, no host wait) overlaps step i+1's K2 on 147 SMs"}
+    if pipelined:
+        last = d_res[-1].cpu().numpy()
+        pml_v, tvar_v = last[: len(RPS)], last[8: 8 + len(RPS)]
+        # the same step run sequentially (K2 on every SM, then the blocking
+        # order_stats), for the record
+        seq_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(10)]
+        torch.cuda.synchronize(dev)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for i in range(10):
+            seq_pml, _ = step(seq_ev[i])
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        assert list(seq_pml) == list(pml_v), "pipelined and sequential K3 disagree"
+        sequential = {"ms_per_step": s0.elapsed_time(s1) / 10,
+                      "k2_ms": float(np.mean([e[0].elapsed_time(e[1]) for e in seq_ev])),
+                      "k3_ms": float(np.mean([e[2].elapsed_time(e[3]) for e in seq_ev])),
+                      "note": "the same step without pipelining: K2 on all 148 SMs, then the exchange and "
+                              "a blocking K3 on the full grid"}
     if world > 1:
         dist.barrier()
     elapsed_ms = start.elapsed_time(stop)
     k2_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     xchg_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
-    k3_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in evs]))
+    k3_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in evs]))  # pipelined: on the spare SM, overlapped
     mx = (lambda v: max_over_ranks(v, dev)) if world > 1 else (lambda v: v)
     elapsed_max = mx(elapsed_ms)
     phases = {"k2_ms": mx(k2_ms), "exchange_ms": mx(xchg_ms), "k3_ms": mx(k3_ms),
               "exchange": ("allgather_portfolio (16 layer rows + portfolio, one NCCL all-gather)" if workload == "c3"
                            else "allgather_ylt (one NCCL all-gather)") if world > 1 else
               ("k3_rollup of the 16 layers" if workload == "c3" else "none (one GPU)")}
+    if pipelined:
+        phases["pipelined"] = (f"step i's exchange + K3 ({2 * spare} CTAs on the {spare} SM(s) K2 leaves free, stream "
+                               f"`side`, no host wait) overlap step i+1's K2 (the other SMs); k3_ms is that overlapped "
+                               f"K3's duration")
     value = total_trials * args.steps / (elapsed_max / 1e3)
 
     side = {}
@@ -722,6 +814,8 @@ def run_ours(args) -> None:
             "kernel": kernel_name,
         },
         "phases_max_over_ranks": phases,
+        **({"sequential": sequential} if pipelined else {}),
+        **({"pipelined": pipelined_side} if pipelined_side else {}),
         "roofline": roofline(n_local, phases["k2_ms"], kernel_name) if workload != "c3" else dict(
             roofline(n_local, phases["k2_ms"], kernel_name),
             bytes_per_launch=n_local * (compulsory_bytes_per_trial() + 8 * 15),
@@ -780,6 +874,9 @@ def main() -> None:
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full-pass", action="store_true", help="reference arm: skip the one full 1M-trial pass")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="time pipelined steps: step i's exchange + K3 on the SMs K2 leaves free overlap "
+                         "step i+1's K2 (default: one step after another)")
     ap.add_argument("--workload", choices=["c2", "c3", "c4"], default="c2",
                     help="c2: 1M trials per GPU (weak scaling, the headline); c3: the 16-layer portfolio over "
                          "1M trials split across the GPUs; c4: 10M trials split across the GPUs")

@@ -53,6 +53,10 @@ typedef enum {
  * (validated once, e.g. by validate_portfolio); K2 then skips its per-id
  * range check.  Without it an out-of-catalog id raises ARE_ERANGE. */
 #define ARE_FLAG_IDS_VALIDATED 0x100
+/* OR-able field for are_simulate_device: the persistent K2 grid leaves k SMs
+ * (0..255) free, so work queued on another stream (a pipelined caller's K3
+ * of the previous batch, its YLT exchange) runs beside it instead of after. */
+#define ARE_SPARE_SMS(k) ((int32_t)(k) << 12)
 
 typedef struct are_tables_s *are_tables_t;
 typedef struct are_plan_s *are_plan_t;
@@ -226,6 +230,13 @@ int are_order_stats_device(const double *d_losses, int64_t n,
 int are_order_stats_host(const double *losses, int64_t n,
                          const double *rps, int64_t n_rp,
                          double *pml_out, double *tvar_out);
+/* Asynchronous form for pipelined callers (no host synchronisation): 1..8
+ * return periods; d_res (device, 16 doubles) receives pml[r] at r and
+ * tvar[r] at 8 + r, stream-ordered on `stream`; at most max_ctas CTAs
+ * (0: the full grid; 1-2 fit beside a K2 launched with ARE_FLAG_SPARE_SM).
+ * Calls must be ordered on one stream per device. */
+int are_order_stats_async(const double *d_losses, int64_t n, const double *rps, int64_t n_rp, double *d_res,
+                          int32_t max_ctas, void *stream);
 /* are_order_stats_device plus the table's mean and maximum from the same
  * tail pass: mean_max_out[0] = sum / n (double-double sum), mean_max_out[1] =
  * max (NaN if any loss is NaN), as the pricing service reports them

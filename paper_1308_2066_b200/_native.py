@@ -22,6 +22,9 @@ LIB_PATH = os.environ.get("ARE_LIB") or os.path.join(os.path.dirname(os.path.abs
 ARE_OK, ARE_EINVAL, ARE_ERANGE, ARE_ECUDA, ARE_ENOMEM, ARE_EINDEX = range(6)
 VARIANTS = {"auto": 0, "hotset": 1, "dense": 2}
 IDS_VALIDATED = 0x100  # ARE_FLAG_IDS_VALIDATED: every YET id is known to be <= catalog
+def spare_sms(k: int) -> int:
+    """ARE_SPARE_SMS(k): K2 leaves k SMs to concurrent work on another stream."""
+    return (int(k) & 0xFF) << 12
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -104,6 +107,7 @@ SIGNATURES = {
     "are_validate_yet_device": (
         ctypes.c_int, [_P, _I64, _P, _I64, _I64, _P, _I64, _I64, ctypes.POINTER(YetReport), _P]),
     "are_order_stats_device": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _P]),
+    "are_order_stats_async": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _I32, _P]),
     "are_order_stats_host": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P]),
     "are_order_stats_summary_device": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _P, _P]),
     "are_pml_many_device": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P]),

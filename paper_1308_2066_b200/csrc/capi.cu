@@ -753,7 +753,11 @@ int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ
         a.rslots = p->rb.rslots;
         a.rfilter = rfilter;
     }
-    return k2_launch(a, v, di->sms, p->smem, (cudaStream_t)stream);
+    // ARE_SPARE_SMS(k): the persistent grid leaves k SMs to concurrent work
+    // on another stream (a pipelined caller's K3 / exchange)
+    const int spare = (v >> 12) & 0xFF;
+    const int sms = std::max(1, di->sms - spare);
+    return k2_launch(a, v, sms, p->smem, (cudaStream_t)stream);
 }
 
 }  // extern "C"
@@ -1033,6 +1037,15 @@ int are_order_stats_device(const double *d_losses, int64_t n, const double *rps,
     DeviceInfo *di;
     if ((rc = use_device(dev, &di))) return rc;
     return k3_order_stats(d_losses, n, rps, n_rp, pml_out, tvar_out, di->sms, (cudaStream_t)stream);
+}
+
+int are_order_stats_async(const double *d_losses, int64_t n, const double *rps, int64_t n_rp, double *d_res,
+                          int32_t max_ctas, void *stream) {
+    int dev, rc;
+    if ((rc = current_device(&dev))) return rc;
+    DeviceInfo *di;
+    if ((rc = use_device(dev, &di))) return rc;
+    return k3_order_stats_async(d_losses, n, rps, n_rp, d_res, di->sms, max_ctas, (cudaStream_t)stream);
 }
 
 int are_order_stats_summary_device(const double *d_losses, int64_t n, const double *rps, int64_t n_rp,

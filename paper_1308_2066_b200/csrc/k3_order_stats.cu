@@ -397,14 +397,12 @@ struct K3Cache {
 };
 static K3Cache g_k3[64];
 
-int k3_order_stats(const double *d_x, int64_t n, const double *rps, int64_t n_rp, double *pml_out,
-                   double *tvar_out, int sms, cudaStream_t st, double *summary) {
-    if (n <= 0) return fail(ARE_EINVAL, "empty year loss table");
-    if (n >= (int64_t)0xFFFFFFFFll) return fail(ARE_EINVAL, "year loss table too long for K3");
-    int dev;
-    ARE_CUDA(cudaGetDevice(&dev));
-    K3Cache &c = g_k3[dev & 63];
-    std::lock_guard<std::mutex> guard(c.mu);
+static K3Cache g_k3_async[64];  // the asynchronous entry's own workspace (one stream per device)
+
+// One K3 launch (<= K3_GROUP return periods) on `st`: clear the work area,
+// the cooperative select, no host synchronisation.
+static int k3_launch(K3Cache &c, const double *d_x, int64_t n, const double *rps, int64_t n_rp, bool summary,
+                     int sms, int max_ctas, cudaStream_t st) {
     constexpr size_t smem = sizeof(unsigned int) * K3_GROUP * K3_BINS;
     if (!c.d_work) {
         ARE_CUDA(cudaFuncSetAttribute(k3_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -416,35 +414,67 @@ int k3_order_stats(const double *d_x, int64_t n, const double *rps, int64_t n_rp
         ARE_CUDA(cudaMalloc(&c.d_part, sizeof(TailPartial) * (size_t)c.grid * (K3_GROUP + 1)));
         ARE_CUDA(cudaHostAlloc(&c.h_res, sizeof(double) * (2 * K3_GROUP + 2), cudaHostAllocDefault));
     }
+    K3Params prm{};
+    prm.n_rp = (int)n_rp;
+    prm.summary = summary;
+    for (int r = 0; r < prm.n_rp; ++r) {
+        int64_t k;
+        int rc = order_stat_k(n, rps[r], &k);
+        if (rc) return rc;
+        prm.rank[r] = k;
+        prm.m_tail[r] = n - k + 1;
+    }
+    ARE_CUDA(cudaMemsetAsync(c.d_work, 0, offsetof(K3Work, res), st));
+    int grid = (int)std::min<int64_t>(c.grid, (n + K3_THREADS - 1) / K3_THREADS);
+    if (max_ctas > 0) grid = std::min(grid, max_ctas);
+    grid = std::max(grid, 1);
+    void *args[] = {(void *)&d_x, (void *)&n, (void *)&prm, (void *)&c.d_work, (void *)&c.d_part};
+    ARE_CUDA(cudaLaunchCooperativeKernel((void *)k3_select, grid, K3_THREADS, args, smem, st));
+    ARE_LAUNCHED();
+    return ARE_OK;
+}
+
+int k3_order_stats(const double *d_x, int64_t n, const double *rps, int64_t n_rp, double *pml_out,
+                   double *tvar_out, int sms, cudaStream_t st, double *summary) {
+    if (n <= 0) return fail(ARE_EINVAL, "empty year loss table");
+    if (n >= (int64_t)0xFFFFFFFFll) return fail(ARE_EINVAL, "year loss table too long for K3");
+    int dev;
+    ARE_CUDA(cudaGetDevice(&dev));
+    K3Cache &c = g_k3[dev & 63];
+    std::lock_guard<std::mutex> guard(c.mu);
     for (int64_t base = 0; base < std::max<int64_t>(n_rp, summary ? 1 : 0); base += K3_GROUP) {
-        K3Params prm{};
-        prm.n_rp = (int)std::min<int64_t>(K3_GROUP, n_rp - base);
-        prm.summary = summary && base == 0;
-        for (int r = 0; r < prm.n_rp; ++r) {
-            int64_t k;
-            int rc = order_stat_k(n, rps[base + r], &k);
-            if (rc) return rc;
-            prm.rank[r] = k;
-            prm.m_tail[r] = n - k + 1;
-        }
-        ARE_CUDA(cudaMemsetAsync(c.d_work, 0, offsetof(K3Work, res), st));
-        int grid = (int)std::min<int64_t>(c.grid, (n + K3_THREADS - 1) / K3_THREADS);
-        grid = std::max(grid, 1);
-        void *args[] = {(void *)&d_x, (void *)&n, (void *)&prm, (void *)&c.d_work, (void *)&c.d_part};
-        ARE_CUDA(cudaLaunchCooperativeKernel((void *)k3_select, grid, K3_THREADS, args, smem, st));
-        ARE_LAUNCHED();
+        const int64_t nr = std::min<int64_t>(K3_GROUP, n_rp - base);
+        int rc = k3_launch(c, d_x, n, rps + base, nr > 0 ? nr : 0, summary && base == 0, sms, 0, st);
+        if (rc) return rc;
         ARE_CUDA(cudaMemcpyAsync(c.h_res, c.d_work->res, sizeof(double) * (2 * K3_GROUP + 2), cudaMemcpyDeviceToHost,
                                  st));
         ARE_CUDA(cudaStreamSynchronize(st));
-        for (int r = 0; r < prm.n_rp; ++r) {
+        for (int r = 0; r < nr; ++r) {
             pml_out[base + r] = c.h_res[r];
             tvar_out[base + r] = c.h_res[K3_GROUP + r];
         }
-        if (prm.summary) {
+        if (summary && base == 0) {
             summary[0] = c.h_res[2 * K3_GROUP];
             summary[1] = c.h_res[2 * K3_GROUP + 1];
         }
     }
+    return ARE_OK;
+}
+
+int k3_order_stats_async(const double *d_x, int64_t n, const double *rps, int64_t n_rp, double *d_res, int sms,
+                         int max_ctas, cudaStream_t st) {
+    if (n <= 0) return fail(ARE_EINVAL, "empty year loss table");
+    if (n >= (int64_t)0xFFFFFFFFll) return fail(ARE_EINVAL, "year loss table too long for K3");
+    if (n_rp < 1 || n_rp > K3_GROUP) return fail(ARE_EINVAL, "asynchronous K3 takes 1..8 return periods");
+    if (!d_res) return fail(ARE_EINVAL, "null result buffer");
+    int dev;
+    ARE_CUDA(cudaGetDevice(&dev));
+    K3Cache &c = g_k3_async[dev & 63];
+    std::lock_guard<std::mutex> guard(c.mu);
+    int rc = k3_launch(c, d_x, n, rps, n_rp, false, sms, max_ctas, st);
+    if (rc) return rc;
+    // pml at d_res[r], tvar at d_res[8 + r]: one device copy, stream-ordered
+    ARE_CUDA(cudaMemcpyAsync(d_res, c.d_work->res, sizeof(double) * 2 * K3_GROUP, cudaMemcpyDeviceToDevice, st));
     return ARE_OK;
 }
 

@@ -216,7 +216,7 @@ class DeviceYearEventTable:
         return None if self.host is None else getattr(self.host, "timestamps", None)
 
     def simulate_device(self, plan, terms, first: int = 0, last: int | None = None, out=None,
-                        stream=None, variant: str = "auto", check: bool = True):
+                        stream=None, variant: str = "auto", check: bool = True, flags: int = 0):
         """K2 over trials [first, last) into a float64 CUDA tensor (allocated
         when `out` is None); launches on `stream` (default: torch's current)."""
         torch = _torch()
@@ -232,7 +232,7 @@ class DeviceYearEventTable:
             int(first), int(last), float(terms.occ_retention), float(terms.occ_limit),
             float(terms.agg_retention), float(terms.agg_limit), out.data_ptr(),
             ctypes.c_void_p(st.cuda_stream),
-            _native.VARIANTS[variant] | flag))
+            _native.VARIANTS[variant] | flag | int(flags)))
         if check and not flag:  # validated ids cannot raise the range flag
             _native.check(lib.are_check_errors(plan.value, ctypes.c_void_p(st.cuda_stream)))
         return out

@@ -110,6 +110,27 @@ def pml_many(ylt, return_periods: Sequence[float], stream=None) -> np.ndarray:
     return out
 
 
+def order_stats_async(d_ylt, return_periods: Sequence[float], d_res, stream, max_ctas: int = 0) -> None:
+    """K3 without a host wait, for pipelined callers: pml[r] lands in d_res[r]
+    and tvar[r] in d_res[8 + r] (a float64 CUDA tensor of >= 16), ordered on
+    `stream`; at most `max_ctas` CTAs (0: the full grid).  One stream per
+    device for every asynchronous call (they share a workspace)."""
+    n = int(d_ylt.shape[0])
+    if n == 0:
+        raise ValueError("empty year loss table")
+    rps = np.ascontiguousarray([float(r) for r in return_periods], dtype=np.float64)
+    _check_rps(n, rps)
+    if not 1 <= rps.size <= 8:
+        raise ValueError("order_stats_async takes 1..8 return periods")
+    import torch
+
+    if d_res.dtype != torch.float64 or d_res.numel() < 16:
+        raise ValueError("d_res must be a float64 CUDA tensor of at least 16 values")
+    _native.check(_native.load().are_order_stats_async(d_ylt.data_ptr(), n, rps.ctypes.data, rps.size,
+                                                       d_res.data_ptr(), int(max_ctas),
+                                                       ctypes.c_void_p(stream.cuda_stream)))
+
+
 def order_stats_summary(d_ylt, return_periods: Sequence[float], stream=None):
     """(pml, tvar, mean, max) from one K3 call over a float64 CUDA tensor: the
     mean and maximum ride along in the tail pass (the pricing service's

@@ -156,3 +156,33 @@ def test_summary_mean_and_max_ride_in_k3(rng):
     y[5] = np.nan
     _, _, mean, peak = order_stats_summary(torch.from_numpy(y).cuda(), [10.0])
     assert np.isnan(mean) and np.isnan(peak)
+
+
+@pytest.mark.parametrize("max_ctas", [0, 2, 16])
+def test_async_k3_on_a_few_ctas_matches(rng, max_ctas):
+    """are_order_stats_async (pipelined callers: K3 on the SMs K2 leaves free,
+    no host wait) against the blocking K3 and numpy: PML exact, TVaR rel
+    1e-12 (its partial sums combine over a different grid)."""
+    import torch
+
+    from paper_1308_2066_b200.risk import order_stats_async
+
+    x = np.minimum(rng.lognormal(8.0, 2.0, 300_001), 66_000.0)
+    x[rng.integers(0, x.size, 500)] = 0.0
+    d = torch.from_numpy(x).cuda()
+    rps = [10.0, 50.0, 100.0, 250.0, 2.0]
+    res = torch.zeros(16, dtype=torch.float64, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    order_stats_async(d, rps, res, side, max_ctas=max_ctas)
+    side.synchronize()
+    got = res.cpu().numpy()
+    p, t = order_stats(d, rps)
+    for r, rp in enumerate(rps):
+        assert got[r] == p[r] == oracle.pml(x, rp)
+        ref = oracle.tvar(x, rp)
+        assert abs(got[8 + r] - ref) <= 1e-12 * abs(ref)
+    with pytest.raises(ValueError):
+        order_stats_async(d, [10.0] * 9, res, side)
+    with pytest.raises(ValueError):
+        order_stats_async(d, [0.5], res, side)
