@@ -291,8 +291,10 @@ int are_yet_free(are_yet_t y);
 /* K2 over trials [first, last) on every shard's GPU at once (the reference's
  * _run_layer, engine/__init__.py:162-201); out_host[t] for t in range,
  * *lookups = n_sel * occurrences.  With n_rp > 0 (whole table only) the
- * slices are also gathered into the first member's HBM (peer copies) and K3
- * evaluates pml/tvar there (metrics.py:29-63).  out_host may be NULL. */
+ * YLT is gathered into the first member's HBM and K3 evaluates pml/tvar
+ * there (metrics.py:29-63): with peer access every shard's K2 stores its
+ * trials straight into that table (the gather fused into the simulation),
+ * else the slices are peer-copied.  out_host may be NULL. */
 int are_run_layer(are_yet_t y, const are_plan_t *plans, int32_t n_plans,
                   double occ_ret, double occ_lim, double agg_ret, double agg_lim,
                   int64_t first, int64_t last, double *out_host, int64_t *lookups, int32_t variant,

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -84,6 +85,7 @@ struct YetShard {
     int64_t *d_off = nullptr;     // offsets t0 .. t1 (absolute occurrence indices)
     double *d_out = nullptr;      // the shard's YLT slice
     unsigned int *d_err = nullptr;
+    cudaEvent_t done = nullptr;   // the shard's K2 has finished (fused gather)
     are_yet_report_t rep{};
 };
 
@@ -107,6 +109,7 @@ static void yet_release(are_yet_s *y) {
         cudaFree(sh.d_out);
         cudaFree(sh.d_err);
         if (sh.stream) cudaStreamDestroy(sh.stream);
+        if (sh.done) cudaEventDestroy(sh.done);
     }
     if (!y->shards.empty() && y->d_full) {
         cudaSetDevice(y->shards[0].device);
@@ -287,6 +290,7 @@ int are_yet_upload(const uint32_t *ids, int64_t n_occ, const int64_t *offsets, i
         int r = use_device(sh.device, &di);
         if (r) return r;
         ARE_CUDA(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking));  // owned by the shard
+        ARE_CUDA(cudaEventCreateWithFlags(&sh.done, cudaEventDisableTiming));
         const int64_t nid = sh.o1 - sh.o0, nt = sh.t1 - sh.t0;
         ARE_CUDA(cudaMalloc(&sh.d_ids, (nid + 4) * sizeof(uint32_t)));
         ARE_CUDA(cudaMalloc(&sh.d_off, (nt + 1) * sizeof(int64_t)));
@@ -362,6 +366,30 @@ int are_yet_free(are_yet_t y) {
     return ARE_OK;
 }
 
+// Can kernels on `from` store into `to`'s memory?  Enables peer access once
+// per pair (a process-wide setting; idempotent).
+static bool peer_store_ok(int from, int to) {
+    static std::mutex mu;
+    static int state[64][64];  // 0 unknown, 1 ok, 2 no
+    if (from < 0 || to < 0 || from >= 64 || to >= 64) return false;
+    std::lock_guard<std::mutex> g(mu);
+    if (!state[from][to]) {
+        int can = 0;
+        DeviceGuard dg;
+        if (cudaDeviceCanAccessPeer(&can, from, to) == cudaSuccess && can) {
+            cudaSetDevice(from);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            state[from][to] = (e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled) ? 1 : 2;
+            if (state[from][to] == 2) cudaGetLastError();
+        } else {
+            cudaGetLastError();
+            state[from][to] = 2;
+        }
+    }
+    return state[from][to] == 1;
+}
+
 int are_run_layer(are_yet_t y, const are_plan_t *plans, int32_t n_plans, double occ_ret, double occ_lim,
                   double agg_ret, double agg_lim, int64_t first, int64_t last, double *out_host, int64_t *lookups,
                   int32_t variant, const double *rps, int64_t n_rp, double *pml_out, double *tvar_out) {
@@ -382,16 +410,60 @@ int are_run_layer(are_yet_t y, const are_plan_t *plans, int32_t n_plans, double 
     DeviceGuard dg;
     std::lock_guard<std::mutex> guard(y->mu);
     const double mean_len = (double)(y->offsets[last] - y->offsets[first]) / (double)(last - first);
-    // K2 on every GPU (asynchronous launches), then each slice straight to
-    // its own range of the caller's output
     int rc = ARE_OK;
+    YetShard &s0 = y->shards[0];
+    // With return periods the YLT is gathered on shard 0's GPU for K3.  When
+    // every shard's GPU can store into that GPU's memory (peer access over
+    // NVLink, or the same device), the gather is fused into K2: each trial's
+    // fold writes its loss straight into the gathered table, so the exchange
+    // overlaps the simulation trial by trial and no copy follows it.
+    bool fused = false;
+    if (n_rp > 0) {
+        ARE_CUDA(cudaSetDevice(s0.device));
+        if (!y->d_full) ARE_CUDA(cudaMalloc(&y->d_full, y->n_trials * sizeof(double)));
+        static const bool no_fuse = [] {  // ARE_GROUP_NO_FUSE=1: the peer-copy gather (A/B, tests)
+            const char *e = getenv("ARE_GROUP_NO_FUSE");
+            return e && e[0] == '1';
+        }();
+        fused = !no_fuse;
+        for (auto &sh : y->shards)
+            if (sh.t1 > sh.t0 && sh.device != s0.device && !peer_store_ok(sh.device, s0.device)) fused = false;
+    }
+    // K2 on every GPU (asynchronous launches), each into its slice (or, fused,
+    // into the gathered table)
     for (auto &sh : y->shards) {
         const int64_t a = std::max(first, sh.t0), b = std::min(last, sh.t1);
         if (a >= b) continue;
         const int s = (int)(&sh - y->shards.data());
         if ((rc = simulate_range(plans[s], sh.d_ids, sh.o0, sh.o1 - sh.o0, sh.d_off, sh.t0, a, b, mean_len, occ_ret,
-                                 occ_lim, agg_ret, agg_lim, sh.d_out, sh.t0, sh.d_err, sh.stream, variant)))
+                                 occ_lim, agg_ret, agg_lim, fused ? y->d_full : sh.d_out, fused ? 0 : sh.t0,
+                                 sh.d_err, sh.stream, variant)))
             return rc;
+        ARE_CUDA(cudaSetDevice(sh.device));
+        ARE_CUDA(cudaEventRecord(sh.done, sh.stream));
+    }
+    if (fused) {
+        // shard 0's stream waits for every K2 (cross-device events), then one
+        // copy of the gathered table to the caller and K3 on it
+        ARE_CUDA(cudaSetDevice(s0.device));
+        for (auto &sh : y->shards)
+            if (sh.t1 > sh.t0 && &sh != &s0) ARE_CUDA(cudaStreamWaitEvent(s0.stream, sh.done, 0));
+        if (out_host)
+            ARE_CUDA(cudaMemcpyAsync(out_host + first, y->d_full + first, (last - first) * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s0.stream));
+        unsigned int bad = 0;
+        for (auto &sh : y->shards) {
+            ARE_CUDA(cudaSetDevice(sh.device));
+            unsigned int h = 0;
+            ARE_CUDA(cudaMemcpyAsync(&h, sh.d_err, sizeof h, cudaMemcpyDeviceToHost, sh.stream));
+            ARE_CUDA(cudaStreamSynchronize(sh.stream));
+            if (h) ARE_CUDA(cudaMemsetAsync(sh.d_err, 0, sizeof(unsigned int), sh.stream));
+            bad |= h;
+        }
+        if (bad) return fail(ARE_ERANGE, "event id outside the catalog in the year event table");
+        DeviceInfo *di;
+        if ((rc = use_device(s0.device, &di))) return rc;
+        return k3_order_stats(y->d_full, y->n_trials, rps, n_rp, pml_out, tvar_out, di->sms, s0.stream);
     }
     for (auto &sh : y->shards) {
         const int64_t a = std::max(first, sh.t0), b = std::min(last, sh.t1);
@@ -411,11 +483,9 @@ int are_run_layer(are_yet_t y, const are_plan_t *plans, int32_t n_plans, double 
     }
     if (bad) return fail(ARE_ERANGE, "event id outside the catalog in the year event table");
     if (n_rp <= 0) return ARE_OK;
-    // gather the slices into the first GPU's memory (peer copies over
-    // NVLink when the slices live on other GPUs), then K3 there
-    YetShard &s0 = y->shards[0];
+    // no peer stores: gather the slices into the first GPU's memory with
+    // peer copies, then K3 there
     ARE_CUDA(cudaSetDevice(s0.device));
-    if (!y->d_full) ARE_CUDA(cudaMalloc(&y->d_full, y->n_trials * sizeof(double)));
     for (auto &sh : y->shards) {
         if (sh.t1 == sh.t0) continue;
         ARE_CUDA(cudaMemcpyPeerAsync(y->d_full + sh.t0, s0.device, sh.d_out, sh.device,

@@ -87,6 +87,24 @@ def test_run_layer_c_abi_gathers_for_k3():
     assert np.all(part[:1000] == -1.0) and np.all(part[4100:] == -1.0)
 
 
+def test_run_layer_gather_paths_agree():
+    """With return periods the shards' K2 store each trial's loss straight
+    into the table gathered on the first GPU (peer stores, fused gather);
+    ARE_GROUP_NO_FUSE=1 runs the peer-copy gather instead.  Both must give
+    the single-GPU YLT and order statistics (the check above, in a fresh
+    process with the variable set)."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, ARE_GROUP_NO_FUSE="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
+                        "tests/test_gpu_group.py::test_run_layer_c_abi_gathers_for_k3"],
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_sharded_k0_report_equals_reference_fixture():
     """The merged per-shard K0 report reproduces the reference's
     validate_portfolio text (tests/golden/validation.json.gz)."""
