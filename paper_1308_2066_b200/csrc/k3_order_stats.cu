@@ -493,6 +493,80 @@ __global__ void k3_gather_ranks(const uint64_t *__restrict__ sorted, const int64
         out[r] = key_value(sorted[ranks[r] - 1]);
 }
 
+// Split keys for the two-pass EP sort: the high and low 32 bits of each
+// order-preserving key; the pairs are sorted by the high half only (4 radix
+// passes instead of 8), which orders every key except inside runs of equal
+// high halves (losses within ~1e-6 of each other, or exactly equal).
+__global__ void k3_keys_split(const double *__restrict__ x, int64_t n, uint32_t *__restrict__ hi,
+                              uint32_t *__restrict__ lo) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = order_key(x[i]);
+        hi[i] = (uint32_t)(k >> 32);
+        lo[i] = (uint32_t)k;
+    }
+}
+// One warp per requested rank: the run of equal high halves around it, then
+// the rank's low half inside the run (all equal -- ties at a cap -- needs
+// nothing more; a short run is resolved by counting; a run longer than
+// K3_RUN_MAX sets *fallback and the host re-sorts the full 64-bit keys).
+static constexpr int64_t K3_RUN_MAX = 256;
+__global__ void k3_select_split(const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo, int64_t n,
+                                const int64_t *__restrict__ ranks, int n_rp, double *__restrict__ out,
+                                unsigned int *__restrict__ fallback) {
+    const int lane = threadIdx.x & 31;
+    const int r = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (r >= n_rp) return;
+    const int64_t k = ranks[r] - 1;  // 0-based position in sorted order
+    const uint32_t h = hi[k];
+    // a run of one (the usual case for distinct losses): no search
+    if ((k == 0 || hi[k - 1] != h) && (k + 1 == n || hi[k + 1] != h)) {
+        if (lane == 0) out[r] = key_value(((uint64_t)h << 32) | lo[k]);
+        return;
+    }
+    // run [s, e) of high half h: binary searches (every lane the same)
+    int64_t a = 0, b = k;
+    while (a < b) {
+        const int64_t m = (a + b) >> 1;
+        if (hi[m] < h) a = m + 1; else b = m;
+    }
+    const int64_t s = a;
+    a = k + 1;
+    b = n;
+    while (a < b) {
+        const int64_t m = (a + b) >> 1;
+        if (hi[m] <= h) a = m + 1; else b = m;
+    }
+    const int64_t e = a, len = e - s;
+    uint32_t lmin = 0xFFFFFFFFu, lmax = 0u;
+    for (int64_t i = s + lane; i < e; i += 32) {
+        lmin = min(lmin, lo[i]);
+        lmax = max(lmax, lo[i]);
+    }
+    lmin = __reduce_min_sync(0xffffffffu, lmin);
+    lmax = __reduce_max_sync(0xffffffffu, lmax);
+    uint32_t want = lmin;
+    if (lmin != lmax) {
+        if (len > K3_RUN_MAX) {
+            if (lane == 0) atomicOr(fallback, 1u);
+            return;
+        }
+        // the low half with exactly (k - s) smaller ones before it in the run
+        const int64_t target = k - s;
+        want = 0xFFFFFFFFu;
+        for (int64_t i = s + lane; i < e; i += 32) {
+            const uint32_t v = lo[i];
+            int64_t less = 0, leq = 0;
+            for (int64_t j = s; j < e; ++j) {
+                less += lo[j] < v;
+                leq += lo[j] <= v;
+            }
+            if (less <= target && target < leq) want = v;
+        }
+        want = __reduce_min_sync(0xffffffffu, want);
+    }
+    if (lane == 0) out[r] = key_value(((uint64_t)h << 32) | want);
+}
+
 struct SortCache {
     std::mutex mu;
     int64_t cap = 0;         // keys
@@ -526,9 +600,12 @@ int k3_pml_sorted(const double *d_x, int64_t n, const double *rps, int64_t n_rp,
         c.d_keys = nullptr;
         c.d_tmp = nullptr;
         c.cap = 0;
-        size_t tmp = 0;
+        size_t tmp = 0, tmp2 = 0;
         ARE_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, (const uint64_t *)nullptr, (uint64_t *)nullptr, n));
-        ARE_CUDA(cudaMalloc(&c.d_keys, sizeof(uint64_t) * 2 * (size_t)n));
+        ARE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                                 (const uint32_t *)nullptr, (uint32_t *)nullptr, n));
+        tmp = std::max(tmp, tmp2);
+        ARE_CUDA(cudaMalloc(&c.d_keys, sizeof(uint64_t) * 2 * (size_t)n));  // or 4 x n uint32 (split)
         ARE_CUDA(cudaMalloc(&c.d_tmp, tmp));
         c.tmp_bytes = tmp;
         c.cap = n;
@@ -544,9 +621,9 @@ int k3_pml_sorted(const double *d_x, int64_t n, const double *rps, int64_t n_rp,
         c.h_out = nullptr;
         c.rank_cap = 0;
         ARE_CUDA(cudaMalloc(&c.d_ranks, sizeof(int64_t) * (size_t)n_rp));
-        ARE_CUDA(cudaMalloc(&c.d_out, sizeof(double) * (size_t)n_rp));
+        ARE_CUDA(cudaMalloc(&c.d_out, sizeof(double) * (size_t)(n_rp + 1)));  // + the fallback flag
         ARE_CUDA(cudaHostAlloc(&c.h_ranks, sizeof(int64_t) * (size_t)n_rp, cudaHostAllocDefault));
-        ARE_CUDA(cudaHostAlloc(&c.h_out, sizeof(double) * (size_t)n_rp, cudaHostAllocDefault));
+        ARE_CUDA(cudaHostAlloc(&c.h_out, sizeof(double) * (size_t)(n_rp + 1), cudaHostAllocDefault));
         c.rank_cap = n_rp;
     }
     // every copy from/to pinned staging, the ranks first: nothing waits on the
@@ -554,15 +631,31 @@ int k3_pml_sorted(const double *d_x, int64_t n, const double *rps, int64_t n_rp,
     std::memcpy(c.h_ranks, ranks.data(), sizeof(int64_t) * (size_t)n_rp);
     ARE_CUDA(cudaMemcpyAsync(c.d_ranks, c.h_ranks, sizeof(int64_t) * (size_t)n_rp, cudaMemcpyHostToDevice, st));
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
-    k3_keys<<<blocks, 256, 0, st>>>(d_x, n, c.d_keys);
-    ARE_LAUNCHED();
     size_t tmp = c.tmp_bytes;
-    ARE_CUDA(cub::DeviceRadixSort::SortKeys(c.d_tmp, tmp, c.d_keys, c.d_keys + c.cap, n, 0, 64, st));
-    k3_gather_ranks<<<(int)std::min<int64_t>((n_rp + 255) / 256, 1024), 256, 0, st>>>(c.d_keys + c.cap, c.d_ranks,
-                                                                                       (int)n_rp, c.d_out);
+    // split keys: sort (high half, low half) pairs by the high half
+    uint32_t *hi_in = reinterpret_cast<uint32_t *>(c.d_keys), *lo_in = hi_in + c.cap;
+    uint32_t *hi_out = lo_in + c.cap, *lo_out = hi_out + c.cap;
+    ARE_CUDA(cudaMemsetAsync(c.d_out + n_rp, 0, sizeof(double), st));
+    k3_keys_split<<<blocks, 256, 0, st>>>(d_x, n, hi_in, lo_in);
     ARE_LAUNCHED();
-    ARE_CUDA(cudaMemcpyAsync(c.h_out, c.d_out, sizeof(double) * (size_t)n_rp, cudaMemcpyDeviceToHost, st));
+    ARE_CUDA(cub::DeviceRadixSort::SortPairs(c.d_tmp, tmp, hi_in, hi_out, lo_in, lo_out, n, 0, 32, st));
+    k3_select_split<<<(int)((n_rp * 32 + 255) / 256), 256, 0, st>>>(
+        hi_out, lo_out, n, c.d_ranks, (int)n_rp, c.d_out, reinterpret_cast<unsigned int *>(c.d_out + n_rp));
+    ARE_LAUNCHED();
+    ARE_CUDA(cudaMemcpyAsync(c.h_out, c.d_out, sizeof(double) * (size_t)(n_rp + 1), cudaMemcpyDeviceToHost, st));
     ARE_CUDA(cudaStreamSynchronize(st));
+    if (c.h_out[n_rp] != 0.0) {  // a long run of near-equal losses: the full 64-bit sort
+        tmp = c.tmp_bytes;
+        k3_keys<<<blocks, 256, 0, st>>>(d_x, n, c.d_keys);
+        ARE_LAUNCHED();
+        ARE_CUDA(cub::DeviceRadixSort::SortKeys(c.d_tmp, tmp, c.d_keys, c.d_keys + c.cap, n, 0, 64, st));
+        k3_gather_ranks<<<(int)std::min<int64_t>((n_rp + 255) / 256, 1024), 256, 0, st>>>(c.d_keys + c.cap,
+                                                                                           c.d_ranks, (int)n_rp,
+                                                                                           c.d_out);
+        ARE_LAUNCHED();
+        ARE_CUDA(cudaMemcpyAsync(c.h_out, c.d_out, sizeof(double) * (size_t)n_rp, cudaMemcpyDeviceToHost, st));
+        ARE_CUDA(cudaStreamSynchronize(st));
+    }
     std::memcpy(pml_out, c.h_out, sizeof(double) * (size_t)n_rp);
     return ARE_OK;
 }

@@ -39,3 +39,24 @@ for _ in range(20):
     ep_curve(d, rps)
 e[1].record(); torch.cuda.synchronize()
 print("ep_curve device timeline per call: %.3f ms" % (e[0].elapsed_time(e[1]) / 20))
+# the C entry alone (no Python validation / EPCurve)
+import ctypes
+from paper_1308_2066_b200 import _native
+lib = _native.load()
+rp_arr = np.ascontiguousarray(rps, dtype=np.float64)
+out = np.empty(rp_arr.size)
+st = torch.cuda.current_stream()
+for _ in range(5):
+    lib.are_pml_many_device(d.data_ptr(), d.numel(), rp_arr.ctypes.data, rp_arr.size, out.ctypes.data, ctypes.c_void_p(st.cuda_stream))
+t = []
+for _ in range(50):
+    t0 = time.perf_counter()
+    lib.are_pml_many_device(d.data_ptr(), d.numel(), rp_arr.ctypes.data, rp_arr.size, out.ctypes.data, ctypes.c_void_p(st.cuda_stream))
+    t.append(time.perf_counter() - t0)
+print("are_pml_many_device alone: median %.3f ms" % (np.median(t) * 1e3))
+t = []
+for _ in range(50):
+    t0 = time.perf_counter()
+    torch.sort(d.view(torch.int64)); torch.cuda.synchronize()
+    t.append(time.perf_counter() - t0)
+print("torch.sort + sync wall: median %.3f ms" % (np.median(t) * 1e3))

@@ -186,3 +186,30 @@ def test_async_k3_on_a_few_ctas_matches(rng, max_ctas):
         order_stats_async(d, [10.0] * 9, res, side)
     with pytest.raises(ValueError):
         order_stats_async(d, [0.5], res, side)
+
+
+def test_ep_curve_runs_of_near_equal_losses(rng):
+    """The EP sort orders by the keys' high 32 bits and resolves runs of equal
+    high halves per requested rank: all-equal runs (a cap), short runs of
+    distinct near-equal losses (counted), and long ones (the 64-bit sort
+    fallback) must all give the exact order statistics."""
+    n = 200_000
+
+    def rp_at(arr, value, offset):
+        # a return period whose rank k = n - floor(n / rp) lands `offset` into
+        # the run starting at `value`
+        k = int(np.searchsorted(np.sort(arr), value)) + 1 + offset
+        return n / (n - k + 0.5)
+
+    x = rng.lognormal(6.0, 1.0, n)
+    x[:50_000] = 7_000.0                                   # a tie run
+    x[50_000:50_200] = 3_000.0 + np.arange(200) * 1e-9     # a short run, distinct low bits
+    rps = np.unique(np.concatenate([np.geomspace(1.05, 2e5, 60),
+                                    [rp_at(x, 3_000.0, o) for o in (0, 37, 199)], [rp_at(x, 7_000.0, 10)]]))
+    got = ep_curve(YearLossTable("x", x), rps).points
+    assert list(got) == list(oracle.ep_points(x, rps))
+    assert any(3_000.0 < v < 3_000.001 and v != 3_000.0 for v, _ in got)  # the short run was hit
+    y = x.copy()
+    y[50_000:55_000] = 3_000.0 + np.arange(5_000) * 1e-10  # a long run: the fallback
+    rps_y = np.unique(np.concatenate([rps, [rp_at(y, 3_000.0, o) for o in (1, 2_500, 4_999)]]))
+    assert list(ep_curve(YearLossTable("y", y), rps_y).points) == list(oracle.ep_points(y, rps_y))
