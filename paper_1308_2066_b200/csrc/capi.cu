@@ -716,6 +716,7 @@ int are_plan_free(are_plan_t p) {
     cudaFree(p->pb.ovf);
     cudaFree(p->pb.filter);
     p->rb.release();
+    cudaFree(p->d_lrec);
     for (auto &f : p->occf) cudaFree(f.d);
     tables_release(p->tab);
     delete p;
@@ -821,6 +822,13 @@ int are_simulate_layers_device(are_plan_t p, int32_t n_layers, const uint64_t *m
     DeviceInfo *di;
     if ((rc = use_device(p->device, &di))) return rc;
     cudaStream_t st = (cudaStream_t)stream;
+    {  // the plan's fused-layer records, once (other streams may use them next)
+        std::lock_guard<std::mutex> g(p->relay_mu);
+        if (!p->d_lrec) {
+            if ((rc = k1_build_layer_records(p->pb, p->d_fin, p->tab->row_len, &p->d_lrec, di->sms, st))) return rc;
+            if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_fail(cudaGetLastError(), "fused-layer records");
+        }
+    }
     uint64_t *d_masks = nullptr;
     LayerTerm *d_terms = nullptr;
     ARE_CUDA(cudaMallocAsync((void **)&d_masks, sizeof(uint64_t) * n_layers, st));
@@ -830,6 +838,7 @@ int are_simulate_layers_device(are_plan_t p, int32_t n_layers, const uint64_t *m
     K2Args a{};
     layer_args(p, a, d_event_ids, n_occ, d_offsets, first, last, d_out);
     K2Layers L{n_layers, out_stride, d_masks, d_terms};
+    L.lrec = p->d_lrec;
     rc = k2_layers_launch(a, L, !(flags & ARE_FLAG_IDS_VALIDATED), di->sms, p->smem, st);
     cudaFreeAsync(d_masks, st);
     cudaFreeAsync(d_terms, st);

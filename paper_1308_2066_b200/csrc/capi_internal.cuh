@@ -75,6 +75,7 @@ struct are_plan_s {
     // relay-kernel records and filter (k1_build_relay), built on first use
     std::mutex relay_mu;
     are::RelayBuffers rb;
+    are::LRec *d_lrec = nullptr;  // fused-layer records (pool plans), built on first layered launch
     int64_t rnbits = 0;
     int rhash_mode = 0;
     size_t rsmem = 0;

@@ -77,6 +77,16 @@ __device__ __forceinline__ uint32_t rslot_cnt(double a) {
 }
 __device__ __forceinline__ uint32_t rslot_ovf(double a) { return (uint32_t)__double2loint(a); }
 
+// Fused-layer record (k2_layers.cu), one per event id, 32 bytes: the
+// event's first two pool entries with the financial terms applied by K1 --
+// fa = 0.0 + f_{j0}(x0) (the first partial sum), fb = f_{j1}(x1) -- their pool
+// positions and count (meta = j0 | j1 << 8 | cnt << 16), the raw first loss
+// x0 and the overflow offset of entries 2..cnt (for the general path).
+struct __align__(32) LRec {
+    double fa, fb, x0;
+    uint32_t meta, ovf;
+};
+
 // Financial terms of one selected table (FinancialTerms, model.py:46-66).
 struct __align__(32) Fin {
     double rate, ret, lim, share;

@@ -195,6 +195,48 @@ __global__ void k1_relay_slots(const Slot *__restrict__ slots, const Entry *__re
     }
 }
 
+// Fused-layer records: the financial terms applied once per entry (the same
+// _rn operations K2-L used to apply per occurrence), so K2-L gathers one
+// 32-byte record per hot event and no dependent overflow load for the
+// second entry.
+__global__ void k1_layer_records(const Slot *__restrict__ slots, const Entry *__restrict__ ovf,
+                                 const Fin *__restrict__ fin, int64_t row_len, LRec *__restrict__ out) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < row_len;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const Slot s = slots[e];
+        const uint32_t cnt = s.meta >> 16;
+        LRec r;
+        r.fa = 0.0;
+        r.fb = 0.0;
+        r.x0 = s.x;
+        r.ovf = s.ovf;
+        uint32_t j0 = 0, j1 = 0;
+        if (cnt) {
+            j0 = s.meta & 0xFFFFu;
+            r.fa = __dadd_rn(0.0, fin_term(fin[j0], s.x));
+        }
+        if (cnt >= 2) {
+            const Entry en = ovf[s.ovf];
+            j1 = en.j;
+            r.fb = fin_term(fin[j1], en.x);
+        }
+        r.meta = (j0 & 0xFFu) | ((j1 & 0xFFu) << 8) | (cnt << 16);
+        out[e] = r;
+    }
+}
+
+int k1_build_layer_records(const PlanBuffers &pb, const Fin *d_fin, int64_t row_len, LRec **out, int sms,
+                           cudaStream_t st) {
+    if (cudaMalloc(out, row_len * sizeof(LRec)) != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return fail(ARE_ENOMEM, "device allocation failed while building the fused-layer records");
+    }
+    k1_layer_records<<<grid_for(row_len, 256, sms), 256, 0, st>>>(pb.slots, pb.ovf, d_fin, row_len, *out);
+    ARE_LAUNCHED();
+    return ARE_OK;
+}
+
 // comb of one relay record, in the reference's order (K2 and the filter)
 __device__ __forceinline__ double relay_comb(const RSlot &r, const double *__restrict__ rovf) {
     if (!rslot_complex(r.a)) return __dadd_rn(r.a, r.b);

@@ -29,6 +29,8 @@ struct RelayBuffers {
     }
 };
 
+int k1_build_layer_records(const PlanBuffers &pb, const Fin *d_fin, int64_t row_len, LRec **out, int sms,
+                           cudaStream_t st);
 int k1_build_relay(const PlanBuffers &pb, const Fin *d_fin, int64_t row_len, int64_t filter_bits, RelayBuffers &rb,
                    int sms, cudaStream_t st, bool precombined = false);
 

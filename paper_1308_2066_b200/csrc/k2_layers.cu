@@ -31,6 +31,11 @@
 namespace are {
 
 static constexpr int LQCAP = 128;   // per-warp queue of event ids
+
+// A gathered LRec as loaded: four doubles (the last holds meta | ovf << 32).
+struct LRecRaw {
+    double fa, fb, x0, mo;
+};
 static constexpr int LSUB = 8;      // events per sub-batch
 static constexpr int LPL = K2L_MAX_LAYERS / 4;  // evaluation layers per lane
 
@@ -151,35 +156,40 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
         llim[r] = l < nl ? s_occ_lim[l] : 0.0;
     }
 
-    auto gather = [&](uint32_t qh, uint32_t n) -> Slot {
-        Slot s{0.0, 0u, 0u};
-        if ((uint32_t)si < n) s = ld_slot(a.slots + q[(qh + si) & (LQCAP - 1)], pol_keep);
-        return s;
+    // one 32-byte record per event (k1_layer_records: the first two entries'
+    // financial terms already applied), kept as loaded; lanes past the
+    // sub-batch read the always-empty record 0 (an unconditional load: a
+    // predicated one would be waited on at once)
+    auto gather = [&](uint32_t qh, uint32_t n) -> LRecRaw {
+        const uint32_t e = (uint32_t)si < n ? q[(qh + si) & (LQCAP - 1)] : 0u;
+        LRecRaw r;
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=d"(r.fa), "=d"(r.fb), "=d"(r.x0), "=d"(r.mo)
+                     : "l"(L.lrec + e), "l"(pol_keep));
+        return r;
     };
     // Evaluate a gathered sub-batch of n <= 8 events and fold it per layer.
     // Fast path (warp-uniform): every event of the sub-batch sits in at most
     // two pool tables (~99% of events at C3), so a layer's comb is
     // 0.0 + [j0 in l] f0 + [j1 in l] f1 in pool order (an absent term adds
     // +0.0 to a comb that is never -0: bit-identical to layer_eval).
-    auto finish = [&](const Slot &s, uint32_t n, double &c) {
-        const uint32_t cnt = (uint32_t)si < n ? (s.meta >> 16) : 0u;
+    auto finish = [&](const LRecRaw &s, uint32_t n, double &c) {
+        const uint32_t meta = (uint32_t)__double2loint(s.mo);
+        const uint32_t cnt = (uint32_t)si < n ? (meta >> 16) : 0u;
         if (__all_sync(0xffffffffu, cnt <= 2u)) {
             // the three possible combs (layer sees j0 only, j1 only, both)
             // and, per entry, the layers that see it (bit 4r <-> layer sg + 4r)
             double c10 = 0.0, c01 = 0.0, c11 = 0.0;
             uint32_t m0 = 0, m1 = 0;
             if (cnt) {
-                const uint32_t j0 = s.meta & 0xFFFFu;
-                c10 = __dadd_rn(0.0, fin_term(s_fin[j0], s.x));
+                c10 = s.fa;  // 0.0 + f_{j0}(x0), taken by K1
                 c11 = c10;
-                m0 = s_lbits[j0] >> sg;
+                m0 = s_lbits[meta & 0xFFu] >> sg;
             }
             if (cnt == 2u) {
-                const Entry en = a.ovf[s.ovf];
-                const double f1 = fin_term(s_fin[en.j], en.x);
-                c01 = __dadd_rn(0.0, f1);
-                c11 = __dadd_rn(c10, f1);
-                m1 = s_lbits[en.j] >> sg;
+                c01 = __dadd_rn(0.0, s.fb);
+                c11 = __dadd_rn(c10, s.fb);
+                m1 = s_lbits[(meta >> 8) & 0xFFu] >> sg;
             }
             double *o = occ + si * K2L_MAX_LAYERS;
 #pragma unroll
@@ -193,7 +203,8 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
                 }
             }
         } else if ((uint32_t)si < n) {
-            layer_eval(s, a.ovf, s_fin, s_mask, s_occ_ret, s_occ_lim, nl, sg, occ + si * K2L_MAX_LAYERS);
+            const Slot sl{s.x0, (meta & 0xFFu) | (cnt << 16), (uint32_t)__double2hiint(s.mo)};
+            layer_eval(sl, a.ovf, s_fin, s_mask, s_occ_ret, s_occ_lim, nl, sg, occ + si * K2L_MAX_LAYERS);
         }
         __syncwarp();
         if (lane < nl) {
@@ -232,7 +243,7 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
         double c = 0.0;  // this lane's layer sum
         uint32_t qh = 0, qt = 0;
         bool pending = false;  // a gathered sub-batch not yet evaluated
-        Slot ps{0.0, 0u, 0u};
+        LRecRaw ps{0.0, 0.0, 0.0, 0.0};
 
         // three row buffers rotate by renaming (chunk ch + 2 loads while ch is
         // filtered); the switch keeps one copy of the append/drain code
@@ -282,7 +293,7 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
                 qt += __popc(b);
                 __syncwarp();
                 while (qt - qh >= (uint32_t)LSUB) {
-                    const Slot ns = gather(qh, LSUB);  // in flight while the previous one finishes
+                    const LRecRaw ns = gather(qh, LSUB);  // in flight while the previous one finishes
                     if (pending) finish(ps, LSUB, c);
                     ps = ns;
                     pending = true;
@@ -292,7 +303,7 @@ __global__ void __launch_bounds__(K2L_THREADS, 1) k2_layers(const K2Args a, cons
         }
         {
             const uint32_t n = qt - qh;
-            const Slot ns = gather(qh, n);
+            const LRecRaw ns = gather(qh, n);
             if (pending) finish(ps, LSUB, c);
             if (n) finish(ns, n, c);
         }

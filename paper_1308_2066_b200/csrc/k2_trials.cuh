@@ -78,6 +78,7 @@ struct K2Layers {
     const uint64_t *masks;   // pool-row bitmask per layer
     const LayerTerm *terms;  // per layer
     const double *occ_table = nullptr;  // pre-combined: occ[e * 16 + l] (k1_layer_occ)
+    const LRec *lrec = nullptr;         // exact fused layers: per-event records (k1_layer_records)
 };
 
 // An event id whose filter bit is clear, used for the stream positions
