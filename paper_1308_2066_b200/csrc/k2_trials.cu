@@ -340,7 +340,10 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_hotset(const K2Args a) {
 // flush are shared by the pair.  The float64 sequence per trial is unchanged.
 static constexpr int PH_CAP = 64;  // per-half queue: < 16 pending + 2 rows of 16
 
-template <int HASH, bool CHECK, bool PRE>
+// REC: the launch gathers the relay records (RSlot, k1_relay_slots: the
+// financial terms applied per entry, the first two entries inline) under the
+// relay's per-occurrence-terms filter, instead of the hot-set slots.
+template <int HASH, bool CHECK, bool PRE, bool REC = false>
 __global__ void __launch_bounds__(K2_THREADS, 1) k2_pair(const K2Args a) {
     constexpr int NW = K2_THREADS / 32;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -383,7 +386,11 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_pair(const K2Args a) {
         if ((uint32_t)idx < n) ev = q[(qh + idx) & (PH_CAP - 1)];
         __syncwarp();
         Slot s{0.0, 0u, 0u};
-        if ((uint32_t)idx < n) s = ld_slot(a.slots + ev, pol_keep);
+        if (REC) {  // the 16-byte relay record, read as a Slot (x = a, meta|ovf = b)
+            if ((uint32_t)idx < n) s = ld_slot(reinterpret_cast<const Slot *>(a.rslots + ev), pol_keep);
+        } else if ((uint32_t)idx < n) {
+            s = ld_slot(a.slots + ev, pol_keep);
+        }
         return s;
     };
     auto finish = [&](const Slot &s, uint32_t n, double &c) {
@@ -391,7 +398,17 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_pair(const K2Args a) {
         if ((uint32_t)idx < n) {
             const uint32_t cnt = s.meta >> 16;
             double comb = 0.0;
-            if (PRE) {
+            if (REC) {
+                const double ra = s.x, rb = __hiloint2double((int)s.ovf, (int)s.meta);
+                if (!rslot_complex(ra)) {
+                    comb = __dadd_rn(ra, rb);
+                } else {
+                    comb = rb;
+                    const uint32_t rc = rslot_cnt(ra), ro = rslot_ovf(ra);
+#pragma unroll 1
+                    for (uint32_t i = 1; i < rc; ++i) comb = __dadd_rn(comb, a.rovf[ro + i - 1]);
+                }
+            } else if (PRE) {
                 if (cnt) comb = s.x;
             } else {
                 if (cnt) comb = __dadd_rn(0.0, fin_term_soa(s_fs, nsel, s.meta & 0xFFFFu, s.x));
@@ -724,34 +741,42 @@ static int prepare_one() {
                                   k2_max_dynamic_smem()));
     ARE_CUDA(cudaFuncSetAttribute(k2_pair<HASH, CHECK, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   k2_max_dynamic_smem()));
+    if (!PRE)
+        ARE_CUDA(cudaFuncSetAttribute(k2_pair<HASH, CHECK, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      k2_max_dynamic_smem()));
     return ARE_OK;
 }
 
-// k2_pair wins on the shortest trials and loses above ~145 occurrences to
-// the relay kernel (measured, K2 ms per 1e9 ids, C5 J=15, pair vs relay:
-// E=100 3.74 vs 4.08, E=130 3.50 vs 3.64, E=160 3.16 vs 2.97, E=200 3.13 vs
-// 2.53, E=250 3.04 vs 2.53).  Without relay records (no texture) the
-// hot-set kernel runs instead, for which the crossover was 320 (round 1:
-// E=250 3.04 vs 3.19, E=500 2.89 vs 2.73).  ARE_K2_PAIR=0/1 forces a kernel.
-// Between the two crossovers the relay kernel needs enough hot ids to pay for
-// its hand-off: at E=250 it loses below ~6% hot events (C5, J=1/2/4: pair
-// 1.87/1.88/1.97 vs relay 2.19/2.21/2.21 ms) and wins above (J=8: 2.30 vs
-// 2.22, J=15: 3.05 vs 2.53).
-// Below 145 the relay kernel still wins when many ids are hot, down to ~64
-// occurrences (E=100: J=15, 14% hot: pair 3.74 vs relay 4.09 ms; J=32, 27%:
-// 5.42 vs 4.30; J=64: 8.29 vs 5.94.  E=30: J=32 8.14 vs 12.66, J=64 11.61 vs
-// 13.12 -- there the per-trial flush through the fold dominates).
-static constexpr double PAIR_MAX_MEAN_LEN = 145.0;
+// k2_pair (reading the relay records under the relay's filter when they
+// exist) wins on short trials and loses to the relay kernel from a length
+// that falls as more events are hot.  Measured, K2 ms at 1e9 ids, C5 shape,
+// k2_pair over relay records vs relay:
+//   J=4  (few hot)  E=160 2.00 vs 2.74, E=250 1.80 vs 2.08
+//   J=15 (14% hot)  E=200 2.50 vs 2.54, E=250 2.46 vs 2.40
+//   J=32 (27% hot)  E=130 3.83 vs 4.18, E=160 3.67 vs 3.66, E=200 3.65 vs 3.30
+//   J=64 (48% hot)  E=130 5.76 vs 5.90, E=160 5.69 vs 5.48
+// Without relay records the hot-set kernel runs above 320 (round 1: E=250
+// 3.04 vs 3.19, E=500 2.89 vs 2.73).  ARE_K2_PAIR=0/1 forces a kernel.
 static constexpr double PAIR_MAX_MEAN_LEN_HOTSET = 320.0;
+static constexpr double PAIR_MAX_MEAN_LEN_DENSE_HOT = 150.0;  // >= 25% of events hot
+static constexpr double PAIR_MAX_MEAN_LEN_MID_HOT = 220.0;    // 6-25% hot
 static constexpr double RELAY_MIN_HOT_FRAC_MID = 0.06;
-static constexpr double RELAY_MIN_HOT_FRAC_SHORT = 0.20;
-static constexpr double RELAY_MIN_MEAN_LEN_SHORT = 64.0;
+static constexpr double RELAY_HOT_FRAC_DENSE = 0.25;
 static bool use_pair(double mean_len, double limit) {
     static const int force = [] {
         const char *e = getenv("ARE_K2_PAIR");
         return e ? (e[0] == '1' ? 1 : 0) : -1;
     }();
     return force >= 0 ? force == 1 : mean_len <= limit;
+}
+
+// ARE_K2_REC_PAIR=0 keeps k2_pair on the hot-set slots (A/B).
+static bool rec_pair_off() {
+    static const bool off = [] {
+        const char *e = getenv("ARE_K2_REC_PAIR");
+        return e && e[0] == '0';
+    }();
+    return off;
 }
 
 // ARE_DENSE_COOP=0 runs the lane-per-event event-major kernel instead (A/B).
@@ -845,8 +870,9 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
     if (g > sms) g = sms;  // persistent: one CTA per SM (the filter fills shared memory)
     const dim3 grid((unsigned)g), block(K2_THREADS);
     const int sel = a.hash_mode * 2 + (check ? 1 : 0);
-    const double pair_limit = a.hot_frac >= RELAY_MIN_HOT_FRAC_SHORT ? RELAY_MIN_MEAN_LEN_SHORT
-                              : a.hot_frac >= RELAY_MIN_HOT_FRAC_MID ? PAIR_MAX_MEAN_LEN : PAIR_MAX_MEAN_LEN_HOTSET;
+    const double pair_limit = a.hot_frac >= RELAY_HOT_FRAC_DENSE ? PAIR_MAX_MEAN_LEN_DENSE_HOT
+                              : a.hot_frac >= RELAY_MIN_HOT_FRAC_MID ? PAIR_MAX_MEAN_LEN_MID_HOT
+                                                                      : PAIR_MAX_MEAN_LEN_HOTSET;
     if (a.rslots && (a.rtex || !k2_relay_needs_texture()) && !use_pair(a.mean_len, pair_limit)) {
         // the relay kernel, over its own filter
         K2Args b = a;
@@ -855,6 +881,29 @@ int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStre
         b.nbits = a.rnbits;
         b.hash_mode = a.rhash_mode;
         return k2_relay_launch(b, check, sms, a.rsmem, st);
+    }
+    if (a.rslots && a.rfilter && !rec_pair_off() && use_pair(a.mean_len, PAIR_MAX_MEAN_LEN_HOTSET)) {
+        // short trials with relay records: k2_pair over the relay's records
+        // and its per-occurrence-terms filter (fewer gathers, no financial
+        // terms or dependent overflow load per occurrence)
+        const size_t rsm = k2_hotset_fixed_smem(a.n_sel) + (size_t)a.rfilter_words * 4u;
+        if (rsm <= (size_t)k2_max_dynamic_smem()) {
+            K2Args b = a;
+            b.filter = a.rfilter;
+            b.filter_words = a.rfilter_words;
+            b.nbits = a.rnbits;
+            b.hash_mode = a.rhash_mode;
+            switch (b.hash_mode * 2 + (check ? 1 : 0)) {
+                case 0: k2_pair<0, false, false, true><<<grid, block, rsm, st>>>(b); break;
+                case 1: k2_pair<0, true, false, true><<<grid, block, rsm, st>>>(b); break;
+                case 2: k2_pair<1, false, false, true><<<grid, block, rsm, st>>>(b); break;
+                case 3: k2_pair<1, true, false, true><<<grid, block, rsm, st>>>(b); break;
+                case 4: k2_pair<2, false, false, true><<<grid, block, rsm, st>>>(b); break;
+                default: k2_pair<2, true, false, true><<<grid, block, rsm, st>>>(b); break;
+            }
+            ARE_LAUNCHED();
+            return ARE_OK;
+        }
     }
     if (a.precombined)
         launch_hotset<true>(a, sel, grid, block, smem_bytes, st);

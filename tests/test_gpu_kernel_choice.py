@@ -4,7 +4,8 @@ The library runs k2_pair (two trials per warp) for launches whose mean trial
 is short and the relay kernel otherwise (csrc/k2_trials.cu `use_pair`), so in
 a normal run each parity test exercises one of them.  ARE_K2_PAIR=0/1 forces
 one of the two for the whole process, and ARE_K2_RELAY=0 replaces the relay
-kernel by the legacy k2_hotset; this runs the core parity tests under each in
+kernel by the legacy k2_hotset (and k2_pair then reads the hot-set slots
+instead of the relay records); this runs the core parity tests under each in
 a subprocess so every kernel meets every case.
 """
 
@@ -23,8 +24,8 @@ CASES = ("random_instances or plugin_run_trials or worked or empty_trial or c1_y
          "or large_catalogs or 256_tables or long_and_ragged or instantiations or resident_and_pinned")
 
 
-@pytest.mark.parametrize("force,relay", [("0", "1"), ("0", "0"), ("1", "1")],
-                         ids=["k2_relay", "k2_hotset", "k2_pair"])
+@pytest.mark.parametrize("force,relay", [("0", "1"), ("0", "0"), ("1", "1"), ("1", "0")],
+                         ids=["k2_relay", "k2_hotset", "k2_pair_relay_records", "k2_pair_slots"])
 def test_parity_suite_under_each_kernel(force, relay):
     env = dict(os.environ, ARE_K2_PAIR=force, ARE_K2_RELAY=relay)
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-q",
