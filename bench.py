@@ -372,12 +372,20 @@ def _sector_roofline(kernel: str, kernel_ms: float, trials: int) -> dict | None:
                     "this, not HBM bandwidth, bounds K2 (DESIGN.md section 4)"}
 
 
-def roofline(trials: int, kernel_ms: float, kernel: str) -> dict:
+def roofline(trials: int, kernel_ms: float, kernel: str, packed_id_bytes: int | None = None) -> dict:
     """K2's roofline on the bytes that cross HBM (the verdict's rule: the
     lookups are served from L2 / shared memory by design, so the SURVEY 8(d)
-    lookup-equivalent figure is reported separately, not as `frac`)."""
+    lookup-equivalent figure is reported separately, not as `frac`).
+    `packed_id_bytes`: the launch streamed the packed resident ids
+    (ARE_PACKED_IDS=1), so those bytes replace the uint32 ids."""
     peak, peak_src = _peaks()
     hbm = trials * compulsory_bytes_per_trial()
+    formula = "trials x (4*E + 8 + 8): ids, offset, float64 YLT slot -- the bytes that cross HBM"
+    if packed_id_bytes is not None:
+        hbm = packed_id_bytes + trials * 16
+        formula = ("packed ids (8 bytes per 3 ids, whole 96-id blocks) + trials x (8 + 8): offset, "
+                   "float64 YLT slot -- the bytes that cross HBM")
+        kernel = kernel + " (packed ids)"
     achieved = hbm / (kernel_ms / 1e3) / 1e9
     traffic = _traffic(kernel)
     lk = trials * bytes_per_trial()
@@ -385,7 +393,7 @@ def roofline(trials: int, kernel_ms: float, kernel: str) -> dict:
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "traffic": traffic, "traffic_ratio": (traffic / (hbm / (trials / TRIALS_PER_GPU))) if traffic else None,
         "kernel": kernel, "kernel_ms": kernel_ms, "bytes_per_launch": hbm,
-        "bytes_formula": "trials x (4*E + 8 + 8): ids, offset, float64 YLT slot -- the bytes that cross HBM",
+        "bytes_formula": formula,
         "peak_source": peak_src,
         "traffic_note": "ncu dram__bytes_read+write per 1M-trial launch (profiles/k2_traffic.json); "
                         "traffic_ratio = traffic / bytes_per_launch at 1M trials",
@@ -585,6 +593,9 @@ def run_ours(args) -> None:
     if workload != "c3":
         info = _native.plan_info(plan)  # the relay records are built by the first launch
         kernel_name = "k2_relay" if info.relay else "k2_hotset"
+    packed_bytes = None  # ARE_PACKED_IDS=1: the relay kernel streamed the packed resident ids
+    if workload != "c3" and info.relay and getattr(dyet, "d_packed", None) is not None:
+        packed_bytes = int(dyet.d_packed.numel()) * 8
     if world > 1:
         dist.barrier()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
@@ -816,7 +827,7 @@ def run_ours(args) -> None:
         "phases_max_over_ranks": phases,
         **({"sequential": sequential} if pipelined else {}),
         **({"pipelined": pipelined_side} if pipelined_side else {}),
-        "roofline": roofline(n_local, phases["k2_ms"], kernel_name) if workload != "c3" else dict(
+        "roofline": roofline(n_local, phases["k2_ms"], kernel_name, packed_bytes) if workload != "c3" else dict(
             roofline(n_local, phases["k2_ms"], kernel_name),
             bytes_per_launch=n_local * (compulsory_bytes_per_trial() + 8 * 15),
             achieved=n_local * (compulsory_bytes_per_trial() + 8 * 15) / (phases["k2_ms"] / 1e3) / 1e9,

@@ -146,6 +146,26 @@ int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ
                         double *d_out, void *stream, int32_t variant);
 int are_check_errors(are_plan_t p, void *stream);
 
+/* Packed resident ids (a device data layout for a YET kept in HBM across
+ * calls, as the reference's pricing sessions keep theirs, service.py:169-188):
+ * three 21-bit ids per 64-bit word, 96-id blocks of 32 words, word l of block
+ * b holding occurrences 96b+l, 96b+32+l, 96b+64+l (bits 0-20, 21-41, 42-62;
+ * zero past n_occ).  are_packed_id_words(n) = words to allocate (2/3 of the
+ * uint32 bytes).  are_yet_pack_device builds it on `stream` from validated
+ * ids; an id >= 2^21 ORs 1 into *d_flag (nullable).
+ * are_simulate_device_packed = are_simulate_device reading d_packed instead
+ * of d_event_ids when the relay kernel runs with ARE_FLAG_IDS_VALIDATED and
+ * the plan's catalogue is below 2^21 (otherwise it reads d_event_ids);
+ * results are bit-identical either way. */
+int64_t are_packed_id_words(int64_t n_occ);
+int are_yet_pack_device(int32_t device, const uint32_t *d_event_ids, int64_t n_occ,
+                        uint64_t *d_packed, uint32_t *d_flag, void *stream);
+int are_simulate_device_packed(are_plan_t p, const uint32_t *d_event_ids, const uint64_t *d_packed,
+                               int64_t n_occ, const int64_t *d_offsets, int64_t n_trials,
+                               int64_t first, int64_t last,
+                               double occ_ret, double occ_lim, double agg_ret, double agg_lim,
+                               double *d_out, void *stream, int32_t variant);
+
 /* Fused multi-layer K2 (replaces the per-layer loop of
  * run_aggregate_analysis_with_stats, engine/__init__.py:242-253).  `p` is a
  * pool plan (are_plan_build_pool, <= 64 tables); layer l selects the pool rows

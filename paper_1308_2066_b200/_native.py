@@ -89,6 +89,12 @@ SIGNATURES = {
         [_P, _P, _I64, _P, _I64, _I64, _I64, _D, _D, _D, _D, _P, _P, _I32],
     ),
     "are_check_errors": (ctypes.c_int, [_P, _P]),
+    "are_packed_id_words": (_I64, [_I64]),
+    "are_yet_pack_device": (ctypes.c_int, [_I32, _P, _I64, _P, _P, _P]),
+    "are_simulate_device_packed": (
+        ctypes.c_int,
+        [_P, _P, _P, _I64, _P, _I64, _I64, _I64, _D, _D, _D, _D, _P, _P, _I32],
+    ),
     "are_simulate_layers_device": (
         ctypes.c_int, [_P, _I32, _P, _P, _P, _I64, _P, _I64, _I64, _I64, _P, _I64, _P, _I32]),
     "are_layer_table_build": (ctypes.c_int, [_P, _I32, _P, _P, _P, ctypes.POINTER(_P)]),

@@ -724,9 +724,10 @@ int are_plan_free(are_plan_t p) {
 }
 
 // ---- K2 -------------------------------------------------------------------
-int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ, const int64_t *d_offsets,
-                        int64_t n_trials, int64_t first, int64_t last, double occ_ret, double occ_lim,
-                        double agg_ret, double agg_lim, double *d_out, void *stream, int32_t variant) {
+static int simulate_device(are_plan_t p, const uint32_t *d_event_ids, const uint64_t *d_packed, int64_t n_occ,
+                           const int64_t *d_offsets, int64_t n_trials, int64_t first, int64_t last, double occ_ret,
+                           double occ_lim, double agg_ret, double agg_lim, double *d_out, void *stream,
+                           int32_t variant) {
     DeviceGuard dg;
     if (!p) return fail(ARE_EINVAL, "null plan handle");
     if (first < 0 || last < first || last > n_trials) return fail(ARE_EINVAL, "trial range out of bounds");
@@ -753,12 +754,44 @@ int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ
     if (rfilter) {
         a.rslots = p->rb.rslots;
         a.rfilter = rfilter;
+        // packed ids: only for ids the caller validated against this plan
+        if (d_packed && (variant & ARE_FLAG_IDS_VALIDATED) && p->tab->row_len <= (1u << 21))
+            a.pids = reinterpret_cast<const unsigned long long *>(d_packed);
     }
     // ARE_SPARE_SMS(k): the persistent grid leaves k SMs to concurrent work
     // on another stream (a pipelined caller's K3 / exchange)
     const int spare = (v >> 12) & 0xFF;
     const int sms = std::max(1, di->sms - spare);
     return k2_launch(a, v, sms, p->smem, (cudaStream_t)stream);
+}
+
+int are_simulate_device(are_plan_t p, const uint32_t *d_event_ids, int64_t n_occ, const int64_t *d_offsets,
+                        int64_t n_trials, int64_t first, int64_t last, double occ_ret, double occ_lim,
+                        double agg_ret, double agg_lim, double *d_out, void *stream, int32_t variant) {
+    return simulate_device(p, d_event_ids, nullptr, n_occ, d_offsets, n_trials, first, last, occ_ret, occ_lim, agg_ret,
+                           agg_lim, d_out, stream, variant);
+}
+
+int are_simulate_device_packed(are_plan_t p, const uint32_t *d_event_ids, const uint64_t *d_packed, int64_t n_occ,
+                               const int64_t *d_offsets, int64_t n_trials, int64_t first, int64_t last,
+                               double occ_ret, double occ_lim, double agg_ret, double agg_lim, double *d_out,
+                               void *stream, int32_t variant) {
+    if (!d_packed) return fail(ARE_EINVAL, "null packed id buffer");
+    return simulate_device(p, d_event_ids, d_packed, n_occ, d_offsets, n_trials, first, last, occ_ret, occ_lim,
+                           agg_ret, agg_lim, d_out, stream, variant);
+}
+
+int64_t are_packed_id_words(int64_t n_occ) { return n_occ < 0 ? -1 : packed_id_words(n_occ); }
+
+int are_yet_pack_device(int32_t device, const uint32_t *d_event_ids, int64_t n_occ, uint64_t *d_packed,
+                        uint32_t *d_flag, void *stream) {
+    DeviceGuard dg;
+    if (n_occ < 0 || (n_occ > 0 && (!d_event_ids || !d_packed))) return fail(ARE_EINVAL, "bad packed id arguments");
+    int rc;
+    DeviceInfo *di;
+    if ((rc = use_device(device, &di))) return rc;
+    return k1_pack_ids_launch(d_event_ids, n_occ, reinterpret_cast<unsigned long long *>(d_packed), d_flag, di->sms,
+                              (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -186,8 +186,9 @@ __device__ __forceinline__ void relay_fold(const K2Args &a, int fw, const double
     }
 }
 
-template <int HASH, bool CHECK>
+template <int HASH, bool CHECK, bool PK>
 __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
+    static_assert(!(PK && CHECK), "packed ids are validated ids");
     extern __shared__ __align__(16) unsigned char smem[];
     // the filter at offset 0 (its LDS addresses need no base register)
     uint32_t *s_filter = reinterpret_cast<uint32_t *>(smem);
@@ -302,124 +303,66 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
 #endif
     };
 
-    // A trial's ids are streamed as 128-id chunks aligned to 128-byte lines
-    // (`skew` positions before the trial; `rel` wraps below zero there, so one
-    // unsigned compare bounds both ends).  The next trial's first two chunks
-    // are requested before the current trial's final batch is flushed, so
-    // their latency overlaps that batch's gather.
-    int64_t t = a.first + (int64_t)blockIdx.x * KR_NP + warp;
-    uint32_t len = 0, rel = 0;
-    const uint32_t *p = ids;
-    int nchunks = 0;
-    uint32_t r0[4], r1[4], r2[4];
-    int64_t nlo = 0, nhi = 0;  // the bounds of the warp's next trial
-    auto begin = [&](int64_t lo, int64_t hi) {
-        const int64_t rlo = lo - a.id_base;
-        len = (uint32_t)(hi - lo);
-        const uint32_t skew = (uint32_t)((reinterpret_cast<uintptr_t>(ids + rlo) >> 2) & 31);
-        p = ids + (rlo - skew) + lane;
-        rel = (uint32_t)lane - skew;
-        nchunks = (int)((len + skew + 127) >> 7);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) r0[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream, pad);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) r1[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream, pad);
-    };
-    if (t < a.last) begin(a.offsets[t - a.t_base], a.offsets[t - a.t_base + 1]);
-    for (; t < a.last; t += W) {
-        const int64_t tn = t + W;
-        if (tn < a.last) {  // next trial's bounds, in flight during this trial
-            nlo = a.offsets[tn - a.t_base];
-            nhi = a.offsets[tn - a.t_base + 1];
-        }
-        uint32_t qh = 0, qt = 0;
-        bool pending = false;
-        RRaw ps{};
-
-        auto step = [&](uint32_t (&cur)[4], uint32_t (&fut)[4]) {
-            const uint32_t rel0 = rel - (uint32_t)lane + 256u;  // start of the chunk loaded now, trial-relative
-            if ((int32_t)rel0 >= 0 && rel0 + 128u <= len) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) fut[k] = ld_stream_u32(p + 256 + 32 * k, pol_stream);
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 256 + 32 * k, rel + 256 + 32 * k, len, pol_stream, pad);
-            }
-            uint32_t ev[4], word[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                uint32_t e = cur[k];
-                if (CHECK) {
-                    emax = max(emax, e);
-                    e = min(e, last_id);
-                }
-                ev[k] = e;
-                word[k] = s_filter[relay_hash<HASH>(e, nbits) >> 5];
-            }
-            constexpr int RPD = ARE_KR_ROWDRAIN ? 1 : 2;  // rows per drain check
-#pragma unroll
-            for (int half = 0; half < 4 / RPD; ++half) {
-#pragma unroll
-                for (int k = RPD * half; k < RPD * half + RPD; ++k) {
-                    const bool hot = (word[k] >> (relay_hash<HASH>(ev[k], nbits) & 31)) & 1u;
+    // One row = 32 ids of a trial in trial order, one per lane.  append_row
+    // queues a row's hot ids in order (ballot + predicated STS); drain turns
+    // every full 32-event batch of the queue into a gather (this batch) and a
+    // value + push (the previous batch, whose gather has had a batch of
+    // filtering to land).
+    uint32_t qh = 0, qt = 0;
+    bool pending = false;
+    RRaw ps{};
+    auto append_row = [&](uint32_t e, uint32_t w) {
+        const bool hot = (w >> (relay_hash<HASH>(e, nbits) & 31)) & 1u;
 #if ARE_KR_EXP == 1  // timing experiment: filter only
-                    emax += hot;
-                    continue;
+        emax += hot;
+        return;
 #endif
-                    const uint32_t b = ballot_full(hot);
-                    st_shared_if(q_saddr + (((qt + __popc(b & lt)) & (KR_QCAP - 1)) << 2), ev[k], hot);
-                    qt += __popc(b);
-                }
-                __syncwarp();
-                while (qt - qh >= 32u) {
+        const uint32_t b = ballot_full(hot);
+        st_shared_if(q_saddr + (((qt + __popc(b & lt)) & (KR_QCAP - 1)) << 2), e, hot);
+        qt += __popc(b);
+    };
+    auto drain = [&]() {
+        __syncwarp();
+        while (qt - qh >= 32u) {
 #if ARE_KR_EXP == 2  // timing experiment: filter + append, no batches
-                    qh += 32u;
-                    continue;
+            qh += 32u;
+            continue;
 #endif
-                    // the pending batch's value first, then the new gather into
-                    // the same registers: no register copy of an in-flight load
-                    const double v = value(ps);
+            // the pending batch's value first, then the new gather into
+            // the same registers: no register copy of an in-flight load
+            const double v = value(ps);
 #if ARE_KR_EXP == 5  // timing experiment: gather, no value, no push
-                    emax ^= (uint32_t)__double2loint(ps.a) ^ (uint32_t)__double2hiint(ps.b);
-                    ps = gather(qh, 32u);
-                    qh += 32u;
-                    continue;
+            emax ^= (uint32_t)__double2loint(ps.a) ^ (uint32_t)__double2hiint(ps.b);
+            ps = gather(qh, 32u);
+            qh += 32u;
+            continue;
 #endif
 #if ARE_KR_EXP == 6  // timing experiment: value of the queued ids (no gather), no push
-                    {
-                        const double v6 = value(ps);
-                        if (v6 == 12345.0) emax++;
-                        const uint32_t e6 = q[(qh + lane) & (KR_QCAP - 1)];
-                        ps = RRaw{(double)e6, 0.0};
-                        qh += 32u;
-                        continue;
-                    }
+            {
+                const double v6 = value(ps);
+                if (v6 == 12345.0) emax++;
+                const uint32_t e6 = q[(qh + lane) & (KR_QCAP - 1)];
+                ps = RRaw{(double)e6, 0.0};
+                qh += 32u;
+                continue;
+            }
 #endif
 #if ARE_KR_EXP == 3  // timing experiment: no push
-                    ps = gather(qh, 32u);
-                    if (v == 12345.0) emax++;
-                    pending = true;
-                    qh += 32u;
-                    continue;
+            ps = gather(qh, 32u);
+            if (v == 12345.0) emax++;
+            pending = true;
+            qh += 32u;
+            continue;
 #endif
-                    ps = gather(qh, 32u);
-                    if (pending) push(v, 0u);
-                    pending = true;
-                    qh += 32u;
-                }
-            }
-            p += 128;
-            rel += 128;
-        };
-        for (int ch = 0; ch < nchunks; ch += 3) {
-            step(r0, r2);
-            if (ch + 1 >= nchunks) break;
-            step(r1, r0);
-            if (ch + 2 >= nchunks) break;
-            step(r2, r1);
+            ps = gather(qh, 32u);
+            if (pending) push(v, 0u);
+            pending = true;
+            qh += 32u;
         }
-        if (tn < a.last) begin(nlo, nhi);  // the next trial's first chunks, in flight during the flush
-        const uint32_t n = qt - qh;  // final partial batch
+    };
+    // the trial's final partial batch, then its end marker
+    auto flush = [&]() {
+        const uint32_t n = qt - qh;
         const double v = value(ps);
         if (n) {
             ps = gather(qh, n);
@@ -427,6 +370,155 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
             push(value(ps), 1u);
         } else {
             push(pending ? v : 0.0, 1u);
+        }
+        qh = qt = 0;
+        pending = false;
+    };
+    constexpr int RPD = ARE_KR_ROWDRAIN ? 1 : 2;  // rows per drain check
+
+    int64_t t = a.first + (int64_t)blockIdx.x * KR_NP + warp;
+    uint32_t len = 0, rel = 0;
+    int nchunks = 0;
+    int64_t nlo = 0, nhi = 0;  // the bounds of the warp's next trial
+    if constexpr (!PK) {
+        // A trial's ids are streamed as 128-id chunks aligned to 128-byte lines
+        // (`skew` positions before the trial; `rel` wraps below zero there, so one
+        // unsigned compare bounds both ends).  The next trial's first two chunks
+        // are requested before the current trial's final batch is flushed, so
+        // their latency overlaps that batch's gather.
+        const uint32_t *p = ids;
+        uint32_t r0[4], r1[4], r2[4];
+        auto begin = [&](int64_t lo, int64_t hi) {
+            const int64_t rlo = lo - a.id_base;
+            len = (uint32_t)(hi - lo);
+            const uint32_t skew = (uint32_t)((reinterpret_cast<uintptr_t>(ids + rlo) >> 2) & 31);
+            p = ids + (rlo - skew) + lane;
+            rel = (uint32_t)lane - skew;
+            nchunks = (int)((len + skew + 127) >> 7);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) r0[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream, pad);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) r1[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream, pad);
+        };
+        if (t < a.last) begin(a.offsets[t - a.t_base], a.offsets[t - a.t_base + 1]);
+        for (; t < a.last; t += W) {
+            const int64_t tn = t + W;
+            if (tn < a.last) {  // next trial's bounds, in flight during this trial
+                nlo = a.offsets[tn - a.t_base];
+                nhi = a.offsets[tn - a.t_base + 1];
+            }
+            auto step = [&](uint32_t (&cur)[4], uint32_t (&fut)[4]) {
+                const uint32_t rel0 = rel - (uint32_t)lane + 256u;  // start of the chunk loaded now, trial-relative
+                if ((int32_t)rel0 >= 0 && rel0 + 128u <= len) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) fut[k] = ld_stream_u32(p + 256 + 32 * k, pol_stream);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 256 + 32 * k, rel + 256 + 32 * k, len, pol_stream, pad);
+                }
+                uint32_t ev[4], word[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    uint32_t e = cur[k];
+                    if (CHECK) {
+                        emax = max(emax, e);
+                        e = min(e, last_id);
+                    }
+                    ev[k] = e;
+                    word[k] = s_filter[relay_hash<HASH>(e, nbits) >> 5];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    append_row(ev[k], word[k]);
+                    if ((k + 1) % RPD == 0) drain();
+                }
+                p += 128;
+                rel += 128;
+            };
+            for (int ch = 0; ch < nchunks; ch += 3) {
+                step(r0, r2);
+                if (ch + 1 >= nchunks) break;
+                step(r1, r0);
+                if (ch + 2 >= nchunks) break;
+                step(r2, r1);
+            }
+            if (tn < a.last) begin(nlo, nhi);  // the next trial's first chunks, in flight during the flush
+            flush();
+        }
+    } else {
+        // Packed resident ids (are_yet_pack_device): three 21-bit ids per
+        // 64-bit word, 96-id blocks of 32 words, word l of a block holding
+        // block positions l, l+32, l+64 -- so one LDG.64 per lane brings three
+        // 32-id rows that are each in lane order, and the in-order append is
+        // unchanged.  A chunk is two blocks (192 ids, 6 rows); two chunks are
+        // in flight while one is filtered.  2/3 of the id sectors of the
+        // uint32 stream (K2 is bound by the SM's sector throughput, §4).
+        const unsigned long long *pp = a.pids;
+        unsigned long long r0[2], r1[2], r2[2];
+        int32_t bleft = 0;  // the trial's blocks from the current chunk on
+        auto ldw = [&](const unsigned long long *w, bool ok) -> unsigned long long {
+            unsigned long long r = 0;
+            asm volatile(
+                "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
+                "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%2], %3;\n\t}"
+                : "+l"(r)
+                : "r"((uint32_t)ok), "l"(w), "l"(pol_stream));
+            return r;
+        };
+        auto begin = [&](int64_t lo, int64_t hi) {
+            const uint64_t rlo = (uint64_t)(lo - a.id_base);
+            const uint64_t b0 = rlo / 96u;
+            const uint32_t skew = (uint32_t)(rlo - b0 * 96u);
+            len = (uint32_t)(hi - lo);
+            pp = a.pids + b0 * 32u + lane;
+            rel = (uint32_t)lane - skew;
+            bleft = (int32_t)((len + skew + 95u) / 96u);
+            nchunks = (bleft + 1) >> 1;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) r0[j] = ldw(pp + 32 * j, j < bleft);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) r1[j] = ldw(pp + 64 + 32 * j, 2 + j < bleft);
+        };
+        if (t < a.last) begin(a.offsets[t - a.t_base], a.offsets[t - a.t_base + 1]);
+        for (; t < a.last; t += W) {
+            const int64_t tn = t + W;
+            if (tn < a.last) {
+                nlo = a.offsets[tn - a.t_base];
+                nhi = a.offsets[tn - a.t_base + 1];
+            }
+            auto step = [&](unsigned long long (&cur)[2], unsigned long long (&fut)[2]) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) fut[j] = ldw(pp + 128 + 32 * j, 4 + j < bleft);
+                uint32_t ev[6], word[6];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const uint32_t lo32 = (uint32_t)cur[j], hi32 = (uint32_t)(cur[j] >> 32);
+                    const uint32_t x[3] = {lo32 & 0x1FFFFFu, __funnelshift_r(lo32, hi32, 21) & 0x1FFFFFu, hi32 >> 10};
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const uint32_t e = rel + (uint32_t)(96 * j + 32 * k) < len ? x[k] : pad;
+                        ev[3 * j + k] = e;
+                        word[3 * j + k] = s_filter[relay_hash<HASH>(e, nbits) >> 5];
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    append_row(ev[k], word[k]);
+                    if ((k + 1) % RPD == 0) drain();
+                }
+                pp += 64;
+                rel += 192;
+                bleft -= 2;
+            };
+            for (int ch = 0; ch < nchunks; ch += 3) {
+                step(r0, r2);
+                if (ch + 1 >= nchunks) break;
+                step(r1, r0);
+                if (ch + 2 >= nchunks) break;
+                step(r2, r1);
+            }
+            if (tn < a.last) begin(nlo, nhi);
+            flush();
         }
     }
 #if ARE_KR_EXP
@@ -437,13 +529,18 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
 
 bool k2_relay_needs_texture() { return ARE_KR_TEX != 0; }
 
+template <int HASH, bool CHECK, bool PK>
+static int relay_attr() {
+    ARE_CUDA(cudaFuncSetAttribute(k2_relay<HASH, CHECK, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
+    return ARE_OK;
+}
+
 int k2_relay_prepare() {
-    ARE_CUDA(cudaFuncSetAttribute(k2_relay<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
-    ARE_CUDA(cudaFuncSetAttribute(k2_relay<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
-    ARE_CUDA(cudaFuncSetAttribute(k2_relay<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
-    ARE_CUDA(cudaFuncSetAttribute(k2_relay<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
-    ARE_CUDA(cudaFuncSetAttribute(k2_relay<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
-    ARE_CUDA(cudaFuncSetAttribute(k2_relay<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2_max_dynamic_smem()));
+    int rc;
+    if ((rc = relay_attr<0, false, false>()) || (rc = relay_attr<0, true, false>()) || (rc = relay_attr<1, false, false>()) ||
+        (rc = relay_attr<1, true, false>()) || (rc = relay_attr<2, false, false>()) || (rc = relay_attr<2, true, false>()) ||
+        (rc = relay_attr<0, false, true>()) || (rc = relay_attr<1, false, true>()) || (rc = relay_attr<2, false, true>()))
+        return rc;
     return ARE_OK;
 }
 
@@ -453,15 +550,57 @@ int k2_relay_launch(const K2Args &a, bool check, int sms, size_t smem_bytes, cud
     int64_t g = (trials + KR_NP - 1) / KR_NP;
     if (g > sms) g = sms;  // persistent: one CTA per SM (the filter fills shared memory)
     const dim3 grid((unsigned)g), block(K2R_THREADS);
+    if (a.pids && !check) {  // packed resident ids (validated by construction)
+        switch (a.hash_mode) {
+            case 0: k2_relay<0, false, true><<<grid, block, smem_bytes, st>>>(a); break;
+            case 1: k2_relay<1, false, true><<<grid, block, smem_bytes, st>>>(a); break;
+            default: k2_relay<2, false, true><<<grid, block, smem_bytes, st>>>(a); break;
+        }
+        ARE_LAUNCHED();
+        return ARE_OK;
+    }
     const int sel = a.hash_mode * 2 + (check ? 1 : 0);
     switch (sel) {
-        case 0: k2_relay<0, false><<<grid, block, smem_bytes, st>>>(a); break;
-        case 1: k2_relay<0, true><<<grid, block, smem_bytes, st>>>(a); break;
-        case 2: k2_relay<1, false><<<grid, block, smem_bytes, st>>>(a); break;
-        case 3: k2_relay<1, true><<<grid, block, smem_bytes, st>>>(a); break;
-        case 4: k2_relay<2, false><<<grid, block, smem_bytes, st>>>(a); break;
-        default: k2_relay<2, true><<<grid, block, smem_bytes, st>>>(a); break;
+        case 0: k2_relay<0, false, false><<<grid, block, smem_bytes, st>>>(a); break;
+        case 1: k2_relay<0, true, false><<<grid, block, smem_bytes, st>>>(a); break;
+        case 2: k2_relay<1, false, false><<<grid, block, smem_bytes, st>>>(a); break;
+        case 3: k2_relay<1, true, false><<<grid, block, smem_bytes, st>>>(a); break;
+        case 4: k2_relay<2, false, false><<<grid, block, smem_bytes, st>>>(a); break;
+        default: k2_relay<2, true, false><<<grid, block, smem_bytes, st>>>(a); break;
     }
+    ARE_LAUNCHED();
+    return ARE_OK;
+}
+
+// Packed resident ids: word b*32 + l of block b holds positions 96b + l,
+// 96b + 32 + l, 96b + 64 + l in bits [0,21), [21,42), [42,63) (zero past
+// n_ids).  Ids >= 2^21 cannot be packed: they set *err (the caller validated
+// the YET, so this is a contract check).
+__global__ void k1_pack_ids(const uint32_t *__restrict__ ids, int64_t n_ids, unsigned long long *__restrict__ pk,
+                            int64_t n_words, unsigned int *err) {
+    bool bad = false;
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n_words; w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t base = (w >> 5) * 96 + (w & 31);
+        unsigned long long v = 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int64_t i = base + 32 * k;
+            const uint32_t e = i < n_ids ? __ldcs(ids + i) : 0u;
+            bad |= e > 0x1FFFFFu;
+            v |= (unsigned long long)(e & 0x1FFFFFu) << (21 * k);
+        }
+        __stcs(pk + w, v);
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0 && err) atomicOr(err, 1u);
+}
+
+int k1_pack_ids_launch(const uint32_t *ids, int64_t n_ids, unsigned long long *pk, unsigned int *err, int sms,
+                       cudaStream_t st) {
+    const int64_t n_words = packed_id_words(n_ids);
+    if (n_words == 0) return ARE_OK;
+    int64_t g = (n_words + 255) / 256;
+    if (g > (int64_t)sms * 8) g = (int64_t)sms * 8;
+    k1_pack_ids<<<(unsigned)g, 256, 0, st>>>(ids, n_ids, pk, n_words, err);
     ARE_LAUNCHED();
     return ARE_OK;
 }

@@ -53,6 +53,9 @@ struct K2Args {
     int32_t rhash_mode = 0;
     size_t rsmem = 0;
     unsigned long long rtex = 0;  // texture object over rslots (uint4 texels), 0: none
+    // packed resident ids (are_yet_pack_device), indexed like `ids`; the relay
+    // kernel streams them instead of `ids` when the ids are validated
+    const unsigned long long *pids = nullptr;
 };
 
 // Threads per CTA of the hot-set kernel (one persistent CTA per SM).
@@ -100,7 +103,11 @@ __device__ __forceinline__ uint32_t cold_pad(const uint32_t *s_filter, int64_t f
 // Largest dynamic shared-memory carve-out requested by K2 (sm_100: 227 KB).
 inline int k2_max_dynamic_smem() { return 227 * 1024; }
 size_t k2_hotset_fixed_smem(int n_sel);
-bool k2_relay_needs_texture();  // the relay build gathers through a texture object
+bool k2_relay_needs_texture();
+// 64-bit words of the packed id layout for n ids (whole 96-id blocks)
+inline int64_t packed_id_words(int64_t n) { return (n + 95) / 96 * 32; }
+int k1_pack_ids_launch(const uint32_t *ids, int64_t n_ids, unsigned long long *pk, unsigned int *err, int sms,
+                       cudaStream_t st);  // the relay build gathers through a texture object
 int k2_prepare(int device);
 int k2_launch(const K2Args &a, int variant, int sms, size_t smem_bytes, cudaStream_t st);
 size_t k2_relay_fixed_smem();

@@ -184,6 +184,86 @@ void run(const uint32_t *ids, const int64_t *off, unsigned long long *sink, int 
            (int)FILTER, (int)GATHER, ms, TRIALS * E * 4 / ms / 1e6, cudaGetErrorString(e));
 }
 
+// MODE 4 (separate kernel): the same per-trial stream over a packed resident
+// layout -- 21-bit ids, three per 64-bit word, stride-major within a 96-id
+// block (lane l's word holds positions l, l+32, l+64), each trial padded to
+// whole blocks.  2.8 GB instead of 4 GB per 1M x 1000 trials.
+constexpr int NBLK = (int)((E + 95) / 96);
+template <int DEPTH, bool GATHER>
+__global__ void __launch_bounds__(NW * 32, 1) stream_packed(const unsigned long long *pk, uint32_t filter_words,
+                                                            unsigned long long *sink, const uint4 *tab) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t *s_f = reinterpret_cast<uint32_t *>(smem);
+    for (uint32_t i = threadIdx.x; i < filter_words; i += blockDim.x)
+        s_f[i] = (i * 2654435761u) & ((i ^ 0x5bd1e995u) * 0x27d4eb2du) & ((i + 0x9e3779b9u) * 0x85ebca6bu);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t acc = 0, pend[3] = {0, 0, 0};
+    auto use = [&](uint32_t e, int k) {
+        const uint32_t hot = ftest(s_f, e);
+        if (!GATHER) { acc += hot; return; }
+        acc += pend[k];
+        uint32_t r = 0;
+        if (hot) r = __ldcg(reinterpret_cast<const unsigned int *>(tab + (e & ((1u << 21) - 1))));
+        pend[k] = r;
+    };
+    const int64_t W = (int64_t)gridDim.x * NW;
+    for (int64_t t = (int64_t)blockIdx.x * NW + warp; t < TRIALS; t += W) {
+        const unsigned long long *base = pk + t * NBLK * 32 + lane;
+        unsigned long long r[DEPTH];
+#pragma unroll
+        for (int d = 0; d < DEPTH; ++d) r[d] = __ldcs(base + 32 * d);
+        for (int c = 0; c < NBLK; c += DEPTH) {
+#pragma unroll
+            for (int d = 0; d < DEPTH; ++d) {
+                const unsigned long long v = r[d];
+                if (c + d + DEPTH < NBLK) r[d] = __ldcs(base + 32 * (c + d + DEPTH));
+                if (c + d < NBLK) {
+                    use((uint32_t)v & 0x1FFFFFu, 0);
+                    use((uint32_t)(v >> 21) & 0x1FFFFFu, 1);
+                    use((uint32_t)(v >> 42), 2);
+                }
+            }
+        }
+    }
+    if (acc == 0x12345678u) sink[0] = acc;
+}
+
+__global__ void pack(const uint32_t *ids, unsigned long long *pk) {
+    const int64_t n = TRIALS * NBLK * 32;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = i / (NBLK * 32), b = (i / 32) % NBLK, l = i % 32;
+        unsigned long long w = 0;
+        for (int k = 0; k < 3; ++k) {
+            const int64_t pos = 96 * b + 32 * k + l;
+            const unsigned long long e = pos < E ? ids[t * E + pos] : 0u;
+            w |= e << (21 * k);
+        }
+        pk[i] = w;
+    }
+}
+
+template <int DEPTH, bool GATHER>
+void run_packed(const unsigned long long *pk, unsigned long long *sink, int sms, const uint4 *tab) {
+    const uint32_t fw = 50000;
+    const size_t smem = fw * 4;
+    cudaFuncSetAttribute(stream_packed<DEPTH, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int i = 0; i < 2; ++i) stream_packed<DEPTH, GATHER><<<sms, NW * 32, smem>>>(pk, fw, sink, tab);
+    cudaEventRecord(a);
+    const int reps = 5;
+    for (int i = 0; i < reps; ++i) stream_packed<DEPTH, GATHER><<<sms, NW * 32, smem>>>(pk, fw, sink, tab);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    ms /= reps;
+    printf("{\"mode\": \"packed21\", \"depth\": %d, \"filter\": 1, \"gather\": %d, \"ms\": %.4f, \"GBps_equiv_u32\": %.1f, \"err\": \"%s\"}\n",
+           DEPTH, (int)GATHER, ms, TRIALS * E * 4 / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+}
+
 int main() {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -200,6 +280,20 @@ int main() {
     uint4 *tab;
     cudaMalloc(&tab, (size_t)(1u << 21) * 16);
     cudaMemset(tab, 0, (size_t)(1u << 21) * 16);
+    if (getenv("PACKED")) {
+        unsigned long long *pk;
+        cudaMalloc(&pk, (size_t)TRIALS * NBLK * 32 * 8);
+        pack<<<sms * 8, 256>>>(ids, pk);
+        run<0, 2, true>(ids, off, sink, sms);
+        run<0, 2, true, true>(ids, off, sink, sms, tab);
+        run<0, 3, true, true>(ids, off, sink, sms, tab);
+        run_packed<2, false>(pk, sink, sms, tab);
+        run_packed<4, false>(pk, sink, sms, tab);
+        run_packed<2, true>(pk, sink, sms, tab);
+        run_packed<3, true>(pk, sink, sms, tab);
+        run_packed<4, true>(pk, sink, sms, tab);
+        return 0;
+    }
     const bool all = getenv("ALL") != nullptr;
     if (all) {
         run<0, 2, false>(ids, off, sink, sms);
