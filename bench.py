@@ -351,6 +351,49 @@ def c3_fused(dyet, stream, reps: int = 5) -> dict:
     return res
 
 
+def packed_side(dyet, plan, terms, d_ref, stream, n: int, k2_ms: float, rest_ms: float) -> dict | None:
+    """K2 of the headline step over the packed resident ids (ARE_PACKED_IDS=1
+    layout, built here beside the uint32 ids and freed after): kernel time,
+    the step rate it implies (same exchange + K3), and frac on the bytes that
+    then cross HBM.  Its YLT must equal the headline's bit for bit."""
+    import torch
+
+    old = os.environ.get("ARE_PACKED_IDS")
+    os.environ["ARE_PACKED_IDS"] = "1"
+    try:
+        dyet._pack_ids()
+    finally:
+        if old is None:
+            os.environ.pop("ARE_PACKED_IDS")
+        else:
+            os.environ["ARE_PACKED_IDS"] = old
+    if dyet.d_packed is None:
+        return None
+    try:
+        out = torch.empty_like(d_ref)
+        for _ in range(3):
+            dyet.simulate_device(plan, terms, out=out, stream=stream, check=False)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(stream)
+        reps = 20
+        for _ in range(reps):
+            dyet.simulate_device(plan, terms, out=out, stream=stream, check=False)
+        ev[1].record(stream)
+        torch.cuda.synchronize(dyet.device)
+        ms = ev[0].elapsed_time(ev[1]) / reps
+        equal = bool(torch.equal(out.view(torch.int64), d_ref.view(torch.int64)))
+        hbm = int(dyet.d_packed.numel()) * 8 + 16 * n
+        peak, _ = _peaks()
+        return {"kernel_ms": ms, "uint32_kernel_ms": k2_ms, "step_trials_per_s": n / ((ms + rest_ms) / 1e3),
+                "bytes_per_launch": hbm, "achieved_gbs": hbm / (ms / 1e3) / 1e9,
+                "frac": hbm / (ms / 1e3) / 1e9 / peak, "ylt_bitwise_equal_headline": equal,
+                "note": "ARE_PACKED_IDS=1: the relay kernel streams three 21-bit ids per 64-bit word "
+                        "(are_yet_pack_device) -- 2/3 of the id bytes, faster K2, lower frac (fewer bytes); "
+                        "opt-in because it keeps a second id copy in HBM (DESIGN.md section 4)"}
+    finally:
+        dyet.d_packed = None
+
+
 def compulsory_bytes_per_trial(events: int = EVENTS) -> int:
     """Bytes that must cross HBM per trial: its ids, its offset, its float64 YLT slot."""
     return 4 * events + 8 + 8
@@ -695,6 +738,10 @@ def run_ours(args) -> None:
             "note": "different unit of work (financial terms folded per event in K1); not the headline"}
         # ---- C3's fused 16-layer pass on this GPU
         side["c3_fused_layers"] = c3_fused(dyet, stream)
+        # ---- the same K2 over the packed resident ids (opt-in layout)
+        if packed_bytes is None and info.relay:
+            side["packed_ids"] = packed_side(dyet, plan, layer.terms, d_local, stream, n_local,
+                                             k2_ms, xchg_ms + k3_ms)
 
     # ---- e2e: the public host API on pinned host buffers --------------------
     # c2: this rank's whole shard; c3/c4: a bounded host sample of it (the

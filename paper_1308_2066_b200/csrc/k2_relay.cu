@@ -66,7 +66,16 @@ namespace are {
 static constexpr int KR_NF = ARE_KR_NF;
 static constexpr int KR_NP = (K2R_THREADS / 32 - KR_NF) / KR_NF * KR_NF;  // producer warps
 static constexpr int KR_PF = KR_NP / KR_NF;                                // producers per fold warp
-static constexpr int KR_QCAP = ARE_KR_ROWDRAIN ? 64 : 128;  // per-producer hot queue (< 32 pending + the rows between drains)
+#ifndef ARE_KR_RPD
+#define ARE_KR_RPD (ARE_KR_ROWDRAIN ? 1 : 2)  // uint32 stream: rows appended between drain checks
+#endif
+#ifndef ARE_KR_RPD_PK
+#define ARE_KR_RPD_PK 3  // packed stream (6 rows per step): rows between drain checks
+#endif
+static constexpr int KR_RPD = ARE_KR_RPD, KR_RPD_PK = ARE_KR_RPD_PK;
+// per-producer hot queue: < 32 pending after a drain + 32 per row appended before the next
+constexpr int kr_qcap(int rows) { return 31 + 32 * rows <= 64 ? 64 : (31 + 32 * rows <= 128 ? 128 : 256); }
+static constexpr int KR_QCAP = kr_qcap(KR_RPD > KR_RPD_PK ? KR_RPD : KR_RPD_PK);
 static constexpr int KR_NB = ARE_KR_NB;                     // batches per ring
 static constexpr int KR_RSTRIDE = KR_NB * 32 + 2;  // doubles per ring (+16 B: the fold's 32 lanes hit distinct banks)
 
@@ -374,7 +383,6 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
         qh = qt = 0;
         pending = false;
     };
-    constexpr int RPD = ARE_KR_ROWDRAIN ? 1 : 2;  // rows per drain check
 
     int64_t t = a.first + (int64_t)blockIdx.x * KR_NP + warp;
     uint32_t len = 0, rel = 0;
@@ -430,7 +438,7 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     append_row(ev[k], word[k]);
-                    if ((k + 1) % RPD == 0) drain();
+                    if ((k + 1) % KR_RPD == 0 || k == 3) drain();
                 }
                 p += 128;
                 rel += 128;
@@ -504,7 +512,7 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
 #pragma unroll
                 for (int k = 0; k < 6; ++k) {
                     append_row(ev[k], word[k]);
-                    if ((k + 1) % RPD == 0) drain();
+                    if ((k + 1) % KR_RPD_PK == 0 || k == 5) drain();
                 }
                 pp += 64;
                 rel += 192;
