@@ -14,6 +14,8 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --mast
 tail -c 300 gpurun_out/bench_torchrun_$TAG.json
 ncu --set full --clock-control none --import-source on -k regex:"k2_(relay|hotset)" -s 1 -c 1 -o gpurun_out/k2_$TAG \
     python scripts/profile_k2.py --launches 2 > gpurun_out/ncu_k2_$TAG.log 2>&1
+ARE_PACKED_IDS=1 ncu --set full --clock-control none --import-source on -k regex:"k2_relay" -s 1 -c 1 -o gpurun_out/k2pk_$TAG \
+    python scripts/profile_k2.py --launches 2 > gpurun_out/ncu_k2pk_$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k3_select -s 2 -c 1 -o gpurun_out/k3_$TAG \
     python scripts/profile_k2.py --launches 3 --k3 > gpurun_out/ncu_k3_$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"^k2_layers$" -s 1 -c 1 -o gpurun_out/k2l_$TAG \
