@@ -15,7 +15,7 @@
 //
 // One persistent CTA of 1024 threads per SM:
 //   * warps 0..30 ("producers") each own trials first + b*31 + w, +31*grid,
-//     ...: they stream the trial's ids (32-id coalesced rows, two 128-id
+//     ...: they stream the trial's ids (32-id coalesced rows, two 192-id
 //     chunks in flight), test each id against the shared-memory filter,
 //     append the hot ones in trial order to a per-warp queue, and per 32
 //     queued events gather one 16-byte record per lane (one LDG.128:
@@ -67,12 +67,16 @@ static constexpr int KR_NF = ARE_KR_NF;
 static constexpr int KR_NP = (K2R_THREADS / 32 - KR_NF) / KR_NF * KR_NF;  // producer warps
 static constexpr int KR_PF = KR_NP / KR_NF;                                // producers per fold warp
 #ifndef ARE_KR_RPD
-#define ARE_KR_RPD (ARE_KR_ROWDRAIN ? 1 : 2)  // uint32 stream: rows appended between drain checks
+#define ARE_KR_RPD (ARE_KR_ROWDRAIN ? 1 : 3)  // uint32 stream: rows appended between drain checks
 #endif
 #ifndef ARE_KR_RPD_PK
 #define ARE_KR_RPD_PK 3  // packed stream (6 rows per step): rows between drain checks
 #endif
+#ifndef ARE_KR_ROWS
+#define ARE_KR_ROWS 6  // uint32 stream: 32-id rows per chunk (two chunks in flight; 4 rows: E=250 2.51 vs 2.43 ms)
+#endif
 static constexpr int KR_RPD = ARE_KR_RPD, KR_RPD_PK = ARE_KR_RPD_PK;
+static constexpr int KR_ROWS = ARE_KR_ROWS, KR_CH = 32 * ARE_KR_ROWS;
 // per-producer hot queue: < 32 pending after a drain + 32 per row appended before the next
 constexpr int kr_qcap(int rows) { return 31 + 32 * rows <= 64 ? 64 : (31 + 32 * rows <= 128 ? 128 : 256); }
 static constexpr int KR_QCAP = kr_qcap(KR_RPD > KR_RPD_PK ? KR_RPD : KR_RPD_PK);
@@ -389,24 +393,24 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
     int nchunks = 0;
     int64_t nlo = 0, nhi = 0;  // the bounds of the warp's next trial
     if constexpr (!PK) {
-        // A trial's ids are streamed as 128-id chunks aligned to 128-byte lines
+        // A trial's ids are streamed as KR_CH-id chunks (6 rows) aligned to 128-byte lines
         // (`skew` positions before the trial; `rel` wraps below zero there, so one
         // unsigned compare bounds both ends).  The next trial's first two chunks
         // are requested before the current trial's final batch is flushed, so
         // their latency overlaps that batch's gather.
         const uint32_t *p = ids;
-        uint32_t r0[4], r1[4], r2[4];
+        uint32_t r0[KR_ROWS], r1[KR_ROWS], r2[KR_ROWS];
         auto begin = [&](int64_t lo, int64_t hi) {
             const int64_t rlo = lo - a.id_base;
             len = (uint32_t)(hi - lo);
             const uint32_t skew = (uint32_t)((reinterpret_cast<uintptr_t>(ids + rlo) >> 2) & 31);
             p = ids + (rlo - skew) + lane;
             rel = (uint32_t)lane - skew;
-            nchunks = (int)((len + skew + 127) >> 7);
+            nchunks = (int)((len + skew + KR_CH - 1) / KR_CH);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) r0[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream, pad);
+            for (int k = 0; k < KR_ROWS; ++k) r0[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream, pad);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) r1[k] = ld_stream_if(p + 128 + 32 * k, rel + 128 + 32 * k, len, pol_stream, pad);
+            for (int k = 0; k < KR_ROWS; ++k) r1[k] = ld_stream_if(p + KR_CH + 32 * k, rel + KR_CH + 32 * k, len, pol_stream, pad);
         };
         if (t < a.last) begin(a.offsets[t - a.t_base], a.offsets[t - a.t_base + 1]);
         for (; t < a.last; t += W) {
@@ -415,18 +419,18 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
                 nlo = a.offsets[tn - a.t_base];
                 nhi = a.offsets[tn - a.t_base + 1];
             }
-            auto step = [&](uint32_t (&cur)[4], uint32_t (&fut)[4]) {
-                const uint32_t rel0 = rel - (uint32_t)lane + 256u;  // start of the chunk loaded now, trial-relative
-                if ((int32_t)rel0 >= 0 && rel0 + 128u <= len) {
+            auto step = [&](uint32_t (&cur)[KR_ROWS], uint32_t (&fut)[KR_ROWS]) {
+                const uint32_t rel0 = rel - (uint32_t)lane + 2u * KR_CH;  // start of the chunk loaded now, trial-relative
+                if ((int32_t)rel0 >= 0 && rel0 + (uint32_t)KR_CH <= len) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) fut[k] = ld_stream_u32(p + 256 + 32 * k, pol_stream);
+                    for (int k = 0; k < KR_ROWS; ++k) fut[k] = ld_stream_u32(p + 2 * KR_CH + 32 * k, pol_stream);
                 } else {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) fut[k] = ld_stream_if(p + 256 + 32 * k, rel + 256 + 32 * k, len, pol_stream, pad);
+                    for (int k = 0; k < KR_ROWS; ++k) fut[k] = ld_stream_if(p + 2 * KR_CH + 32 * k, rel + 2 * KR_CH + 32 * k, len, pol_stream, pad);
                 }
-                uint32_t ev[4], word[4];
+                uint32_t ev[KR_ROWS], word[KR_ROWS];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < KR_ROWS; ++k) {
                     uint32_t e = cur[k];
                     if (CHECK) {
                         emax = max(emax, e);
@@ -436,12 +440,12 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
                     word[k] = s_filter[relay_hash<HASH>(e, nbits) >> 5];
                 }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < KR_ROWS; ++k) {
                     append_row(ev[k], word[k]);
-                    if ((k + 1) % KR_RPD == 0 || k == 3) drain();
+                    if ((k + 1) % KR_RPD == 0 || k == KR_ROWS - 1) drain();
                 }
-                p += 128;
-                rel += 128;
+                p += KR_CH;
+                rel += KR_CH;
             };
             for (int ch = 0; ch < nchunks; ch += 3) {
                 step(r0, r2);
