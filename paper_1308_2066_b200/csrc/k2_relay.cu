@@ -60,6 +60,9 @@ namespace are {
 #ifndef ARE_KR_FOLD_TRYWAIT
 #define ARE_KR_FOLD_TRYWAIT 0  // the fold polls with try_wait (zero suspend hint) instead of test_wait
 #endif
+#ifndef ARE_KR_FOLD_SLEEP
+#define ARE_KR_FOLD_SLEEP 32  // ns the fold warp sleeps when no producer has a batch ready
+#endif
 #ifndef ARE_KR_EXP
 #define ARE_KR_EXP 0       // timing experiments only (results are wrong when != 0)
 #endif
@@ -171,7 +174,7 @@ __device__ __forceinline__ void relay_fold(const K2Args &a, int fw, const double
         bool ready = false;
         if (t < a.last) ready = mbar_test(full + slot * 8, (head / KR_NB) & 1);
         if (!__any_sync(0xffffffffu, ready)) {
-            __nanosleep(32);
+            if (ARE_KR_FOLD_SLEEP) __nanosleep(ARE_KR_FOLD_SLEEP);
             continue;
         }
         if (ready) {
