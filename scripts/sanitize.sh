@@ -22,3 +22,8 @@ compute-sanitizer --tool memcheck --error-exitcode 9 python scripts/relay_small.
 compute-sanitizer --tool synccheck --num-cuda-barriers 40000 --error-exitcode 9 python scripts/relay_small.py 2>&1 | tail -2
 compute-sanitizer --tool racecheck --num-cuda-barriers 40000 --print-limit 4 python scripts/relay_small.py 2>&1 | tail -6
 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_group.py tests/test_gpu_concurrency.py -x -q 2>&1 | tail -3
+# round 2, late: the packed-id stream of the relay kernel (k2_relay<..., PK=true>) and the packing kernel
+compute-sanitizer --tool memcheck --error-exitcode 9 python scripts/relay_small.py --packed 2>&1 | tail -2
+compute-sanitizer --tool synccheck --num-cuda-barriers 40000 --error-exitcode 9 python scripts/relay_small.py --packed 2>&1 | tail -2
+compute-sanitizer --tool racecheck --num-cuda-barriers 40000 --print-limit 4 python scripts/relay_small.py --packed 2>&1 | tail -6
+compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_packed.py -x -q -k "layout or subrange or wide" 2>&1 | tail -3
