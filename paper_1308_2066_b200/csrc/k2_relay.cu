@@ -63,6 +63,9 @@ namespace are {
 #ifndef ARE_KR_FOLD_SLEEP
 #define ARE_KR_FOLD_SLEEP 32  // ns the fold warp sleeps when no producer has a batch ready
 #endif
+#ifndef ARE_KR_BOUNDS
+#define ARE_KR_BOUNDS 0  // debug build: packed-array and queue-capacity checks set bits 2/4 of the plan's error word
+#endif
 #ifndef ARE_KR_EXP
 #define ARE_KR_EXP 0       // timing experiments only (results are wrong when != 0)
 #endif
@@ -336,6 +339,9 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
         const uint32_t b = ballot_full(hot);
         st_shared_if(q_saddr + (((qt + __popc(b & lt)) & (KR_QCAP - 1)) << 2), e, hot);
         qt += __popc(b);
+#if ARE_KR_BOUNDS  // debug build: the ring never holds more than KR_QCAP entries
+        if (qt - qh > (uint32_t)KR_QCAP) atomicOr(a.err, 4u);
+#endif
     };
     auto drain = [&]() {
         __syncwarp();
@@ -473,6 +479,9 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
         int32_t bleft = 0;  // the trial's blocks from the current chunk on
         auto ldw = [&](const unsigned long long *w, bool ok) -> unsigned long long {
             unsigned long long r = 0;
+#if ARE_KR_BOUNDS  // debug build: every packed word read lies inside the packed array
+            if (ok && (uint64_t)(w - a.pids) >= (uint64_t)packed_id_words(a.n_ids)) atomicOr(a.err, 2u);
+#endif
             asm volatile(
                 "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
                 "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%2], %3;\n\t}"

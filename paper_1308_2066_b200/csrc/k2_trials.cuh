@@ -105,7 +105,7 @@ inline int k2_max_dynamic_smem() { return 227 * 1024; }
 size_t k2_hotset_fixed_smem(int n_sel);
 bool k2_relay_needs_texture();
 // 64-bit words of the packed id layout for n ids (whole 96-id blocks)
-inline int64_t packed_id_words(int64_t n) { return (n + 95) / 96 * 32; }
+__host__ __device__ inline int64_t packed_id_words(int64_t n) { return (n + 95) / 96 * 32; }
 int k1_pack_ids_launch(const uint32_t *ids, int64_t n_ids, unsigned long long *pk, unsigned int *err, int sms,
                        cudaStream_t st);  // the relay build gathers through a texture object
 int k2_prepare(int device);
