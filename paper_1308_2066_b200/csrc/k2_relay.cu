@@ -83,6 +83,10 @@ static constexpr int KR_PF = KR_NP / KR_NF;                                // pr
 #endif
 static constexpr int KR_RPD = ARE_KR_RPD, KR_RPD_PK = ARE_KR_RPD_PK;
 static constexpr int KR_ROWS = ARE_KR_ROWS, KR_CH = 32 * ARE_KR_ROWS;
+#ifndef ARE_KR_PKB
+#define ARE_KR_PKB 1  // packed stream: 96-id blocks per chunk (two chunks in flight; 2 blocks: 1.726 vs 1.716 ms)
+#endif
+static constexpr int KR_PKB = ARE_KR_PKB;
 // per-producer hot queue: < 32 pending after a drain + 32 per row appended before the next
 constexpr int kr_qcap(int rows) { return 31 + 32 * rows <= 64 ? 64 : (31 + 32 * rows <= 128 ? 128 : 256); }
 static constexpr int KR_QCAP = kr_qcap(KR_RPD > KR_RPD_PK ? KR_RPD : KR_RPD_PK);
@@ -471,11 +475,11 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
         // 64-bit word, 96-id blocks of 32 words, word l of a block holding
         // block positions l, l+32, l+64 -- so one LDG.64 per lane brings three
         // 32-id rows that are each in lane order, and the in-order append is
-        // unchanged.  A chunk is two blocks (192 ids, 6 rows); two chunks are
-        // in flight while one is filtered.  2/3 of the id sectors of the
-        // uint32 stream (K2 is bound by the SM's sector throughput, §4).
+        // unchanged.  A chunk is KR_PKB blocks (one: 96 ids, 3 rows, one drain
+        // check); two chunks are in flight while one is filtered.  2/3 of the
+        // id sectors of the uint32 stream.
         const unsigned long long *pp = a.pids;
-        unsigned long long r0[2], r1[2], r2[2];
+        unsigned long long r0[KR_PKB], r1[KR_PKB], r2[KR_PKB];
         int32_t bleft = 0;  // the trial's blocks from the current chunk on
         auto ldw = [&](const unsigned long long *w, bool ok) -> unsigned long long {
             unsigned long long r = 0;
@@ -497,11 +501,11 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
             pp = a.pids + b0 * 32u + lane;
             rel = (uint32_t)lane - skew;
             bleft = (int32_t)((len + skew + 95u) / 96u);
-            nchunks = (bleft + 1) >> 1;
+            nchunks = (bleft + KR_PKB - 1) / KR_PKB;
 #pragma unroll
-            for (int j = 0; j < 2; ++j) r0[j] = ldw(pp + 32 * j, j < bleft);
+            for (int j = 0; j < KR_PKB; ++j) r0[j] = ldw(pp + 32 * j, j < bleft);
 #pragma unroll
-            for (int j = 0; j < 2; ++j) r1[j] = ldw(pp + 64 + 32 * j, 2 + j < bleft);
+            for (int j = 0; j < KR_PKB; ++j) r1[j] = ldw(pp + 32 * KR_PKB + 32 * j, KR_PKB + j < bleft);
         };
         if (t < a.last) begin(a.offsets[t - a.t_base], a.offsets[t - a.t_base + 1]);
         for (; t < a.last; t += W) {
@@ -510,12 +514,12 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
                 nlo = a.offsets[tn - a.t_base];
                 nhi = a.offsets[tn - a.t_base + 1];
             }
-            auto step = [&](unsigned long long (&cur)[2], unsigned long long (&fut)[2]) {
+            auto step = [&](unsigned long long (&cur)[KR_PKB], unsigned long long (&fut)[KR_PKB]) {
 #pragma unroll
-                for (int j = 0; j < 2; ++j) fut[j] = ldw(pp + 128 + 32 * j, 4 + j < bleft);
-                uint32_t ev[6], word[6];
+                for (int j = 0; j < KR_PKB; ++j) fut[j] = ldw(pp + 64 * KR_PKB + 32 * j, 2 * KR_PKB + j < bleft);
+                uint32_t ev[3 * KR_PKB], word[3 * KR_PKB];
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
+                for (int j = 0; j < KR_PKB; ++j) {
                     const uint32_t lo32 = (uint32_t)cur[j], hi32 = (uint32_t)(cur[j] >> 32);
                     const uint32_t x[3] = {lo32 & 0x1FFFFFu, __funnelshift_r(lo32, hi32, 21) & 0x1FFFFFu, hi32 >> 10};
 #pragma unroll
@@ -526,13 +530,13 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
                     }
                 }
 #pragma unroll
-                for (int k = 0; k < 6; ++k) {
+                for (int k = 0; k < 3 * KR_PKB; ++k) {
                     append_row(ev[k], word[k]);
-                    if ((k + 1) % KR_RPD_PK == 0 || k == 5) drain();
+                    if ((k + 1) % KR_RPD_PK == 0 || k == 3 * KR_PKB - 1) drain();
                 }
-                pp += 64;
-                rel += 192;
-                bleft -= 2;
+                pp += 32 * KR_PKB;
+                rel += 96 * KR_PKB;
+                bleft -= KR_PKB;
             };
             for (int ch = 0; ch < nchunks; ch += 3) {
                 step(r0, r2);
