@@ -83,10 +83,16 @@ static constexpr int KR_PF = KR_NP / KR_NF;                                // pr
 #endif
 static constexpr int KR_RPD = ARE_KR_RPD, KR_RPD_PK = ARE_KR_RPD_PK;
 static constexpr int KR_ROWS = ARE_KR_ROWS, KR_CH = 32 * ARE_KR_ROWS;
+#ifndef ARE_KR_AHEAD
+#define ARE_KR_AHEAD 2  // uint32 stream: chunks loaded ahead of the one being filtered (2-4)
+#endif
 #ifndef ARE_KR_PKB
 #define ARE_KR_PKB 1  // packed stream: 96-id blocks per chunk (two chunks in flight; 2 blocks: 1.726 vs 1.716 ms)
 #endif
 static constexpr int KR_PKB = ARE_KR_PKB;
+#ifndef ARE_KR_PK_AHEAD
+#define ARE_KR_PK_AHEAD 3  // packed stream: chunks loaded ahead of the one being filtered (2-4; 2: 1.715 vs 1.687 ms)
+#endif
 // per-producer hot queue: < 32 pending after a drain + 32 per row appended before the next
 constexpr int kr_qcap(int rows) { return 31 + 32 * rows <= 64 ? 64 : (31 + 32 * rows <= 128 ? 128 : 256); }
 static constexpr int KR_QCAP = kr_qcap(KR_RPD > KR_RPD_PK ? KR_RPD : KR_RPD_PK);
@@ -413,6 +419,12 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
         // their latency overlaps that batch's gather.
         const uint32_t *p = ids;
         uint32_t r0[KR_ROWS], r1[KR_ROWS], r2[KR_ROWS];
+#if ARE_KR_AHEAD >= 3
+        uint32_t r3[KR_ROWS];
+#endif
+#if ARE_KR_AHEAD >= 4
+        uint32_t r4[KR_ROWS];
+#endif
         auto begin = [&](int64_t lo, int64_t hi) {
             const int64_t rlo = lo - a.id_base;
             len = (uint32_t)(hi - lo);
@@ -424,6 +436,16 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
             for (int k = 0; k < KR_ROWS; ++k) r0[k] = ld_stream_if(p + 32 * k, rel + 32 * k, len, pol_stream, pad);
 #pragma unroll
             for (int k = 0; k < KR_ROWS; ++k) r1[k] = ld_stream_if(p + KR_CH + 32 * k, rel + KR_CH + 32 * k, len, pol_stream, pad);
+#if ARE_KR_AHEAD >= 3
+#pragma unroll
+            for (int k = 0; k < KR_ROWS; ++k)
+                r2[k] = ld_stream_if(p + 2 * KR_CH + 32 * k, rel + 2 * KR_CH + 32 * k, len, pol_stream, pad);
+#endif
+#if ARE_KR_AHEAD >= 4
+#pragma unroll
+            for (int k = 0; k < KR_ROWS; ++k)
+                r3[k] = ld_stream_if(p + 3 * KR_CH + 32 * k, rel + 3 * KR_CH + 32 * k, len, pol_stream, pad);
+#endif
         };
         if (t < a.last) begin(a.offsets[t - a.t_base], a.offsets[t - a.t_base + 1]);
         for (; t < a.last; t += W) {
@@ -433,13 +455,14 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
                 nhi = a.offsets[tn - a.t_base + 1];
             }
             auto step = [&](uint32_t (&cur)[KR_ROWS], uint32_t (&fut)[KR_ROWS]) {
-                const uint32_t rel0 = rel - (uint32_t)lane + 2u * KR_CH;  // start of the chunk loaded now, trial-relative
+                const uint32_t rel0 = rel - (uint32_t)lane + (uint32_t)(ARE_KR_AHEAD * KR_CH);  // start of the chunk loaded now, trial-relative
                 if ((int32_t)rel0 >= 0 && rel0 + (uint32_t)KR_CH <= len) {
 #pragma unroll
-                    for (int k = 0; k < KR_ROWS; ++k) fut[k] = ld_stream_u32(p + 2 * KR_CH + 32 * k, pol_stream);
+                    for (int k = 0; k < KR_ROWS; ++k) fut[k] = ld_stream_u32(p + ARE_KR_AHEAD * KR_CH + 32 * k, pol_stream);
                 } else {
 #pragma unroll
-                    for (int k = 0; k < KR_ROWS; ++k) fut[k] = ld_stream_if(p + 2 * KR_CH + 32 * k, rel + 2 * KR_CH + 32 * k, len, pol_stream, pad);
+                    for (int k = 0; k < KR_ROWS; ++k) fut[k] = ld_stream_if(p + ARE_KR_AHEAD * KR_CH + 32 * k, rel + ARE_KR_AHEAD * KR_CH + 32 * k, len,
+                                              pol_stream, pad);
                 }
                 uint32_t ev[KR_ROWS], word[KR_ROWS];
 #pragma unroll
@@ -460,6 +483,29 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
                 p += KR_CH;
                 rel += KR_CH;
             };
+#if ARE_KR_AHEAD == 4
+            for (int ch = 0; ch < nchunks; ch += 5) {
+                step(r0, r4);
+                if (ch + 1 >= nchunks) break;
+                step(r1, r0);
+                if (ch + 2 >= nchunks) break;
+                step(r2, r1);
+                if (ch + 3 >= nchunks) break;
+                step(r3, r2);
+                if (ch + 4 >= nchunks) break;
+                step(r4, r3);
+            }
+#elif ARE_KR_AHEAD == 3
+            for (int ch = 0; ch < nchunks; ch += 4) {
+                step(r0, r3);
+                if (ch + 1 >= nchunks) break;
+                step(r1, r0);
+                if (ch + 2 >= nchunks) break;
+                step(r2, r1);
+                if (ch + 3 >= nchunks) break;
+                step(r3, r2);
+            }
+#else
             for (int ch = 0; ch < nchunks; ch += 3) {
                 step(r0, r2);
                 if (ch + 1 >= nchunks) break;
@@ -467,6 +513,7 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
                 if (ch + 2 >= nchunks) break;
                 step(r2, r1);
             }
+#endif
             if (tn < a.last) begin(nlo, nhi);  // the next trial's first chunks, in flight during the flush
             flush();
         }
@@ -480,6 +527,12 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
         // id sectors of the uint32 stream.
         const unsigned long long *pp = a.pids;
         unsigned long long r0[KR_PKB], r1[KR_PKB], r2[KR_PKB];
+#if ARE_KR_PK_AHEAD >= 3
+        unsigned long long r3[KR_PKB];
+#endif
+#if ARE_KR_PK_AHEAD >= 4
+        unsigned long long r4[KR_PKB];
+#endif
         int32_t bleft = 0;  // the trial's blocks from the current chunk on
         auto ldw = [&](const unsigned long long *w, bool ok) -> unsigned long long {
             unsigned long long r = 0;
@@ -506,6 +559,14 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
             for (int j = 0; j < KR_PKB; ++j) r0[j] = ldw(pp + 32 * j, j < bleft);
 #pragma unroll
             for (int j = 0; j < KR_PKB; ++j) r1[j] = ldw(pp + 32 * KR_PKB + 32 * j, KR_PKB + j < bleft);
+#if ARE_KR_PK_AHEAD >= 3
+#pragma unroll
+            for (int j = 0; j < KR_PKB; ++j) r2[j] = ldw(pp + 64 * KR_PKB + 32 * j, 2 * KR_PKB + j < bleft);
+#endif
+#if ARE_KR_PK_AHEAD >= 4
+#pragma unroll
+            for (int j = 0; j < KR_PKB; ++j) r3[j] = ldw(pp + 96 * KR_PKB + 32 * j, 3 * KR_PKB + j < bleft);
+#endif
         };
         if (t < a.last) begin(a.offsets[t - a.t_base], a.offsets[t - a.t_base + 1]);
         for (; t < a.last; t += W) {
@@ -516,7 +577,8 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
             }
             auto step = [&](unsigned long long (&cur)[KR_PKB], unsigned long long (&fut)[KR_PKB]) {
 #pragma unroll
-                for (int j = 0; j < KR_PKB; ++j) fut[j] = ldw(pp + 64 * KR_PKB + 32 * j, 2 * KR_PKB + j < bleft);
+                for (int j = 0; j < KR_PKB; ++j)
+                    fut[j] = ldw(pp + 32 * ARE_KR_PK_AHEAD * KR_PKB + 32 * j, ARE_KR_PK_AHEAD * KR_PKB + j < bleft);
                 uint32_t ev[3 * KR_PKB], word[3 * KR_PKB];
 #pragma unroll
                 for (int j = 0; j < KR_PKB; ++j) {
@@ -538,6 +600,29 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
                 rel += 96 * KR_PKB;
                 bleft -= KR_PKB;
             };
+#if ARE_KR_PK_AHEAD == 4
+            for (int ch = 0; ch < nchunks; ch += 5) {
+                step(r0, r4);
+                if (ch + 1 >= nchunks) break;
+                step(r1, r0);
+                if (ch + 2 >= nchunks) break;
+                step(r2, r1);
+                if (ch + 3 >= nchunks) break;
+                step(r3, r2);
+                if (ch + 4 >= nchunks) break;
+                step(r4, r3);
+            }
+#elif ARE_KR_PK_AHEAD == 3
+            for (int ch = 0; ch < nchunks; ch += 4) {
+                step(r0, r3);
+                if (ch + 1 >= nchunks) break;
+                step(r1, r0);
+                if (ch + 2 >= nchunks) break;
+                step(r2, r1);
+                if (ch + 3 >= nchunks) break;
+                step(r3, r2);
+            }
+#else
             for (int ch = 0; ch < nchunks; ch += 3) {
                 step(r0, r2);
                 if (ch + 1 >= nchunks) break;
@@ -545,6 +630,7 @@ __global__ void __launch_bounds__(K2R_THREADS, 1) k2_relay(const K2Args a) {
                 if (ch + 2 >= nchunks) break;
                 step(r2, r1);
             }
+#endif
             if (tn < a.last) begin(nlo, nhi);
             flush();
         }
