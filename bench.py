@@ -2,7 +2,7 @@
 """Benchmark: aggregate-analysis trials/sec on the C2 workload (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c3|c4] [--scaling weak|strong]
+                    [--workload c2|c3|c4] [--scaling weak|strong] [--pipeline] [--packed-ids]
 
 --workload c3 (the 16-layer portfolio over 1M trials split across the GPUs,
 allgather_portfolio between ranks) and c4 / --scaling strong (10M trials
@@ -940,7 +940,13 @@ def main() -> None:
                          "1M trials split across the GPUs; c4: 10M trials split across the GPUs")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="strong = --workload c4 (C4's fixed 10M trials over N GPUs)")
+    ap.add_argument("--packed-ids", action="store_true",
+                    help="keep the resident ids in the packed layout (ARE_PACKED_IDS=1): the relay kernel "
+                         "streams 2/3 of the id bytes; roofline bytes follow (default: uint32 ids, the packed "
+                         "K2 is reported beside as `packed_ids`)")
     args = ap.parse_args()
+    if args.packed_ids:
+        os.environ["ARE_PACKED_IDS"] = "1"
     if args.scaling == "strong" and args.workload == "c2":
         args.workload = "c4"
     if args.warmup < 3:
